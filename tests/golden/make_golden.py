@@ -1,0 +1,146 @@
+"""Generate golden fixtures from the REAL reference (``sparsekv``).
+
+Run in the build container, where ``/root/reference`` exists:
+
+    python tests/golden/make_golden.py
+
+It imports the unmodified reference from ``/root/reference/pkg/src`` and
+drives its public API (``ContextStore`` / ``Session.update`` /
+``Session.attention`` on the DIPR/FLAT plan, ``dipr_bruteforce``,
+``WindowConfig``, ``workload``). Outputs go to ``tests/golden/*.npz``; the
+GPU box never reads ``/root/reference`` -- only these committed fixtures.
+Large inputs are NOT stored: the reference generator is pinned by a sha256
+of its arrays, and the tests regenerate them with the restated generator in
+``oracle/alaya_oracle.py`` and check the hash first.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+OUT = Path(__file__).resolve().parent
+sys.path.insert(0, str(REF))
+sys.path.insert(0, str(OUT.parents[1]))
+
+from sparsekv import (  # noqa: E402
+    ContextStore, EngineConfig, ModelShape, WindowConfig, dipr_bruteforce,
+)
+from sparsekv.workload import WorkloadSpec, decode_step_inputs, make_context  # noqa: E402
+
+from oracle.alaya_oracle import bf16_round  # noqa: E402
+
+
+def sha(*arrays) -> str:
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def flat_session_case(name, n_layers, hq, hkv, d, n, steps, seed, beta, win_init, win_last,
+                      clusters=16, bf16=False, store_inputs=False, layers_checked=None):
+    """Drive the reference session API on the DIPR/FLAT plan and record it."""
+    shape = ModelShape(n_layers, hq, hkv, d)
+    cfg = EngineConfig(beta=beta, window_initial=win_init, window_last=win_last,
+                       first_layers=tuple(range(n_layers)), short_context_threshold=0)
+    spec = WorkloadSpec(n_tokens=n, shape=shape, seed=seed, clusters=clusters)
+    ctx = make_context(spec)
+    keys, values = ctx.keys, ctx.values
+    gen_hash = sha(ctx.token_ids, keys, values, ctx.centers)
+    if bf16:
+        keys, values = bf16_round(keys), bf16_round(values)
+    tids, qs, ks, vs = decode_step_inputs(spec, steps, ctx.centers)
+    step_hash = sha(tids, qs, ks, vs)
+    if bf16:
+        ks, vs = bf16_round(ks), bf16_round(vs)
+    db = ContextStore(shape, cfg)
+    db.import_context(ctx.token_ids, keys, values)
+    session, _ = db.create_session(ctx.token_ids)
+    layers_checked = list(range(n_layers)) if layers_checked is None else layers_checked
+    rec = {"shape": np.array([n_layers, hq, hkv, d, n, steps, seed, clusters]),
+           "beta": np.float64(beta), "window": np.array([win_init, win_last]),
+           "bf16": np.int64(bf16), "layers": np.array(layers_checked)}
+    outs, sel_flat, sel_off, retrieved = [], [], [0], []
+    for step in range(steps):
+        for layer in range(n_layers):
+            session.update(qs[step, layer], ks[step, layer], vs[step, layer], layer)
+        session.record_token(int(tids[step]))
+        for layer in layers_checked:
+            assert session.active_plan(layer).query.value == "dipr"
+            assert session.active_plan(layer).index.value == "flat"
+            o = session.attention(qs[step, layer], layer)
+            outs.append(o)
+            for info in session.last_diagnostics["heads"]:
+                sel_flat.extend(info["selected_base"])
+                sel_off.append(len(sel_flat))
+                retrieved.append(info["retrieved"])
+    rec.update(out=np.stack(outs), sel=np.array(sel_flat, dtype=np.int32),
+               sel_off=np.array(sel_off, dtype=np.int64),
+               retrieved=np.array(retrieved, dtype=np.int64))
+    rec["gen_sha"] = np.array(gen_hash)
+    rec["step_sha"] = np.array(step_hash)
+    if store_inputs:
+        rec.update(keys=keys, values=values, q=qs, k=ks, v=vs)
+    np.savez_compressed(OUT / f"{name}.npz", **rec)
+    print(name, "out", rec["out"].shape, "sel", rec["sel"].size)
+
+
+def known_answers():
+    """Known-answer DIPR / window cases lifted from the reference's own tests."""
+    rng = np.random.default_rng(12345)  # reference tests/conftest.py:7-9
+    cases = {}
+    # tests/test_dipr.py:69-72 hand case
+    q = np.array([1.0, 0.0], dtype=np.float32)
+    keys = np.array([[3.0, 0.0], [2.5, 0.0], [0.0, 1.0]], dtype=np.float32)
+    cases["hand_q"], cases["hand_k"] = q, keys
+    cases["hand_out"] = np.array(sorted(dipr_bruteforce(q, keys, 1.0)))
+    # random DIPR sets over a beta ladder (tests/test_dipr.py:63-98 style)
+    q = rng.standard_normal(64).astype(np.float32) * 3
+    keys = rng.standard_normal((1200, 64)).astype(np.float32) * 3
+    cases["rand_q"], cases["rand_k"] = q, keys
+    betas = np.array([0.0, 1.0, 5.0, 20.0, 50.0, 110.0, 1e9])
+    cases["rand_betas"] = betas
+    flat, off = [], [0]
+    for b in betas:
+        s = sorted(dipr_bruteforce(q, keys, float(b)))
+        flat.extend(s)
+        off.append(len(flat))
+    cases["rand_sel"], cases["rand_off"] = np.array(flat, np.int32), np.array(off)
+    # WindowConfig.base_ids (tests/test_core.py:139-150)
+    wins = []
+    for p, ini, last in [(0, 16, 64), (10, 16, 64), (80, 16, 64), (81, 16, 64),
+                         (4096, 16, 64), (100, 0, 8), (100, 4, 0)]:
+        ids = WindowConfig(ini, last).base_ids(p)
+        wins.append(np.concatenate([[p, ini, last, ids.size], ids]))
+    cases["windows"] = np.concatenate(wins)
+    np.savez_compressed(OUT / "known_answers.npz", **cases)
+    print("known_answers")
+
+
+def main():
+    known_answers()
+    # tiny shapes with stored inputs: edge cases of the window/selection logic
+    flat_session_case("tiny_gqa", 2, 4, 2, 16, 200, 3, seed=1, beta=8.0,
+                      win_init=4, win_last=8, clusters=6, store_inputs=True)
+    flat_session_case("tiny_short", 1, 4, 1, 16, 10, 2, seed=2, beta=8.0,
+                      win_init=4, win_last=8, clusters=3, store_inputs=True)
+    flat_session_case("tiny_nowin", 1, 6, 2, 32, 333, 2, seed=3, beta=30.0,
+                      win_init=0, win_last=0, clusters=4, store_inputs=True)
+    # BASELINE config 1: Llama-3.1-8B layer (32 q / 8 kv, d=128), ctx 4K, fp32
+    flat_session_case("llama_4k_fp32", 1, 32, 8, 128, 4096, 2, seed=0, beta=110.0,
+                      win_init=16, win_last=64)
+    # bf16-rounded K/V variant of the same layer
+    flat_session_case("llama_4k_bf16", 1, 32, 8, 128, 4096, 1, seed=0, beta=110.0,
+                      win_init=16, win_last=64, bf16=True)
+    # Qwen2.5-14B-shaped layer (40 q / 8 kv), smaller ctx, beta 20
+    flat_session_case("qwen_2k_fp32", 1, 40, 8, 128, 2048, 1, seed=5, beta=20.0,
+                      win_init=16, win_last=64)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,84 @@
+"""Pin the CPU oracle against the real reference's golden fixtures (CPU only)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import alaya_oracle as O
+from tests.golden_cases import GOLDEN, SESSION_CASES, load_session_case, window_rows
+
+
+def test_known_answer_hand_case():
+    z = np.load(GOLDEN / "known_answers.npz")
+    got = sorted(O.dipr_bruteforce(z["hand_q"], z["hand_k"], 1.0))
+    assert got == z["hand_out"].tolist() == [0, 1]
+
+
+def test_known_answer_beta_ladder():
+    z = np.load(GOLDEN / "known_answers.npz")
+    off = z["rand_off"]
+    for i, b in enumerate(z["rand_betas"]):
+        want = z["rand_sel"][off[i]:off[i + 1]].tolist()
+        assert sorted(O.dipr_bruteforce(z["rand_q"], z["rand_k"], float(b))) == want
+
+
+def test_known_answer_windows():
+    z = np.load(GOLDEN / "known_answers.npz")["windows"]
+    i = 0
+    while i < z.size:
+        p, ini, last, m = (int(x) for x in z[i:i + 4])
+        want = z[i + 4:i + 4 + m]
+        assert np.array_equal(O.window_base_ids(p, ini, last), want)
+        i += 4 + m
+
+
+def test_dipr_errors():
+    with pytest.raises(ValueError):
+        O.dipr_bruteforce(np.ones(3, np.float32), np.empty((0, 3), np.float32), 1.0)
+    with pytest.raises(ValueError):
+        O.dipr_bruteforce(np.ones(3, np.float32), np.ones((4, 3), np.float32), -0.1)
+
+
+def test_alpha_beta():
+    assert O.alpha_to_beta(1.0, 128) == 0.0
+    assert O.alpha_to_beta(np.exp(-2.0), 64) == pytest.approx(16.0, rel=1e-12)
+    with pytest.raises(ValueError):
+        O.alpha_to_beta(0.0, 8)
+
+
+@pytest.mark.parametrize("name", SESSION_CASES)
+def test_session_attention_bit_exact_vs_reference(name):
+    """The restatement reproduces ``Session.attention`` on the flat plan bit for bit."""
+    c = load_session_case(name)
+    for step in range(c.steps):
+        for li, layer in enumerate(c.layers):
+            wk, wv = window_rows(c, step, layer)
+            out, sels, counts = O.session_attention_flat(
+                c.q[step, layer], c.keys[layer], c.values[layer], wk, wv, c.beta,
+                c.win_init, c.win_last)
+            idx = c.call_index(step, li)
+            assert np.array_equal(out, c.out[idx])
+            for qh in range(c.hq):
+                assert np.array_equal(sels[qh], c.selected(step, li, qh))
+                assert counts[qh] == c.retrieved[idx * c.hq + qh]
+
+
+def test_bf16_round_is_rne():
+    x = np.array([1.0, 1.00390625, 1.0078125 + 2 ** -9, -3.5, 1e-40], dtype=np.float32)
+    r = O.bf16_round(x)
+    assert r[0] == 1.0 and r[1] == 1.0  # tie to even
+    assert r[3] == -3.5
+    import torch
+    t = torch.from_numpy(x).to(torch.bfloat16).float().numpy()
+    assert np.array_equal(r, t)
+
+
+def test_box_bound_is_sound(rng):
+    keys = rng.standard_normal((1000, 32)).astype(np.float32)
+    q = rng.standard_normal(32).astype(np.float32)
+    lo, hi = O.block_box_bounds(keys, 128)
+    ub = O.block_upper_bounds(q, lo, hi)
+    s = O.inner_products(keys, q)
+    for b in range(ub.size):
+        assert s[b * 128:(b + 1) * 128].max() <= ub[b] + 1e-9
