@@ -1,0 +1,149 @@
+/*
+ * alaya.h -- C-ABI of the B200-native DIPR retrieval + sparse-attention path.
+ *
+ * This is the drop-in boundary under the reference's Python surface
+ * (package ``sparsekv``, /root/reference/pkg/src/sparsekv). The reference has
+ * no native code; each entry point below replaces one numeric stage of its
+ * decode step, cited file:line:
+ *
+ *   alaya_dipr_attention   Session.attention on the DIPR/FLAT plan
+ *                          (store.py:191-216 -> _head_attention :252-293,
+ *                          _retrieve flat branch :336-337).
+ *   alaya_scan             inner_products + scores.max()  (core.py:64-67,
+ *                          dipr.py:63-64), batched over GQA groups.
+ *   alaya_attend           mask s >= max - beta (dipr.py:64), setdiff with the
+ *                          window ids (store.py:271-273, core.py:159-165),
+ *                          PartialAttention.over(selected) and .over(window)
+ *                          merged (attention.py:98-143) -> one (m,l,acc) state.
+ *   alaya_merge_partials   PartialAttention.merge + finalize
+ *                          (attention.py:128-152) across sequence shards.
+ *   alaya_selected         dipr_bruteforce's id set (dipr.py:65-70) and the
+ *                          Session.last_diagnostics lists (store.py:288-292).
+ *   alaya_block_bounds_*   sound coarse block filter feeding the scan
+ *                          (input: BlockIndex, index.py:195-243).
+ *
+ * Conventions: every pointer named d_* is DEVICE memory; descriptor arrays and
+ * params are HOST memory read during the call. All work is stream-ordered on
+ * ``stream``; no call synchronises the device. Return value 0 = ok, otherwise
+ * an alaya_status code; alaya_last_error() gives a message (thread-local).
+ * Entry points are reentrant; state lives only in the caller's workspace.
+ */
+#ifndef ALAYA_H_
+#define ALAYA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ALAYA_OK = 0,
+  ALAYA_ERR_ARG = 1,        /* maps to ValueError (store.py:175-178,200-204) */
+  ALAYA_ERR_SHAPE = 2,      /* maps to ValueError */
+  ALAYA_ERR_NONFINITE = 3,  /* maps to FloatingPointError (attention.py:150-151) */
+  ALAYA_ERR_CUDA = 4,
+  ALAYA_ERR_WORKSPACE = 5,
+  ALAYA_ERR_UNSUPPORTED = 6
+} alaya_status;
+
+typedef enum { ALAYA_F32 = 0, ALAYA_BF16 = 1 } alaya_dtype;
+
+typedef enum {
+  ALAYA_SCAN_AUTO = 0,
+  ALAYA_SCAN_CUDA_CORE = 1, /* warp-shuffle q.k on FP32 pipes */
+  ALAYA_SCAN_TCGEN05 = 2    /* bf16 q.K^T on 5th-gen tensor cores (TMEM accum) */
+} alaya_scan_kind;
+
+/* One sequence (session) for one layer.
+ * Base prefix keys of kv head h, token t (local row) live at
+ *   k + (h * head_stride + t * dim) elements; same for v.
+ * Session-window rows (Session.update, store.py:160-189) at
+ *   wk + (h * w_head_stride + r * dim).
+ * Sequence-sharded mode: this shard holds global rows
+ *   [token_offset, token_offset + n) of a base prefix of prefix_len tokens;
+ *   unsharded callers pass token_offset = 0, prefix_len = n. */
+typedef struct {
+  const void* k;
+  const void* v;
+  const void* wk;
+  const void* wv;
+  int64_t head_stride;
+  int64_t w_head_stride;
+  int64_t token_offset;
+  int64_t prefix_len;
+  int32_t n;
+  int32_t w;
+} alaya_seq;
+
+typedef struct {
+  int32_t n_query_heads;
+  int32_t n_kv_heads;
+  int32_t dim;           /* 16, 32, 64, 128 or 256 */
+  int32_t dtype;         /* alaya_dtype of K/V (base and window) */
+  float beta;            /* raw inner-product slack (dipr.py:47-70) */
+  int32_t win_initial;   /* WindowConfig.initial (core.py:152) */
+  int32_t win_last;      /* WindowConfig.last (core.py:153) */
+  int32_t chunk;         /* tokens per work chunk; 0 = auto */
+  int32_t scan_kind;     /* alaya_scan_kind */
+  int32_t block_filter;  /* 1 = skip blocks with a sound UB < LB - beta */
+} alaya_params;
+
+#define ALAYA_MAX_BATCH 128
+#define ALAYA_PARTIAL_STRIDE(dim) ((dim) + 2) /* (m, l, acc[dim]) per query head */
+
+const char* alaya_last_error(void);
+int alaya_version(void);
+
+/* Workspace bytes needed for a call on this batch. */
+size_t alaya_workspace_bytes(const alaya_params* p, const alaya_seq* seqs, int batch);
+
+/* Full single-GPU decode step for one layer over `batch` sequences.
+ * d_q: [batch][Hq][dim] fp32.  d_out: [batch][Hq][dim] fp32. */
+int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch,
+                         const float* d_q, float* d_out, void* d_ws, size_t ws_bytes,
+                         void* stream);
+
+/* Stage 1: score every base key of every query head, per-head max and the
+ * candidate superset. Writes the local max per (seq, q head) to d_smax
+ * ([batch][Hq] fp32, -inf where n == 0); d_smax may be NULL (scan only). */
+int alaya_scan(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q,
+               float* d_smax, void* d_ws, size_t ws_bytes, void* stream);
+
+/* Stage 2: exact filter at d_smax - beta (the GLOBAL max after an allreduce in
+ * sharded mode), V gather + online softmax over the selection, merged with
+ * the window rows this shard owns. Writes one partial state per query head:
+ * d_part[(b*Hq+qh)*(dim+2) + {0:m, 1:l, 2..:acc}] (m = -inf, l = 0 if empty).
+ * want_values = 0 skips the V gather (DIPR-only). */
+int alaya_attend(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q,
+                 const float* d_smax, float* d_part, int want_values, void* d_ws,
+                 size_t ws_bytes, void* stream);
+
+/* Stage 3: merge n_parts partial sets (d_parts: [n_parts][batch*Hq][dim+2]) in
+ * order and finalize to d_out [batch*Hq][dim] fp32. Non-finite output sets
+ * *d_status (device int) to ALAYA_ERR_NONFINITE. */
+int alaya_merge_partials(const float* d_parts, int n_parts, int rows, int dim, float* d_out,
+                         int* d_status, void* stream);
+
+/* PartialAttention.merge without finalize (attention.py:128-143): merge
+ * n_parts state sets in order into d_state [rows][dim+2]. */
+int alaya_merge_states(const float* d_parts, int n_parts, int rows, int dim, float* d_state,
+                       void* stream);
+
+/* After alaya_attend on the same workspace: per (seq, q head) selected ids
+ * (global, ascending) into d_ids[(b*Hq+qh)*cap ...], counts into
+ * d_selected[b*Hq+qh] and the retrieved count (including window ids) into
+ * d_retrieved[b*Hq+qh]. cap must be >= max prefix rows per shard. */
+int alaya_selected(const alaya_params* p, const alaya_seq* seqs, int batch, int64_t* d_ids,
+                   int64_t cap, int32_t* d_selected, int32_t* d_retrieved, void* d_ws,
+                   size_t ws_bytes, void* stream);
+
+/* Device status word of the last alaya_dipr_attention on this workspace
+ * (ALAYA_OK or ALAYA_ERR_NONFINITE); pointer into d_ws. */
+int* alaya_ws_status(void* d_ws);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ALAYA_H_ */

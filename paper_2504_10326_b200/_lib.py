@@ -1,0 +1,119 @@
+"""ctypes binding of the C-ABI in ``include/alaya.h`` (``libalaya_b200.so``).
+
+The library is built in-tree (``paper_2504_10326_b200/csrc/Makefile``) and
+loaded from this package directory. There is no fallback: if the library is
+missing or no CUDA device is present, every compute entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+LIB_NAME = "libalaya_b200.so"
+LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+
+ALAYA_OK = 0
+ALAYA_ERR_ARG = 1
+ALAYA_ERR_SHAPE = 2
+ALAYA_ERR_NONFINITE = 3
+ALAYA_ERR_CUDA = 4
+ALAYA_ERR_WORKSPACE = 5
+ALAYA_ERR_UNSUPPORTED = 6
+
+ALAYA_F32 = 0
+ALAYA_BF16 = 1
+
+SCAN_AUTO = 0
+SCAN_CUDA_CORE = 1
+SCAN_TCGEN05 = 2
+
+MAX_BATCH = 128
+
+# every symbol include/alaya.h declares (checked by tests/test_boundary.py)
+EXPORTS = (
+    "alaya_last_error", "alaya_version", "alaya_workspace_bytes", "alaya_dipr_attention",
+    "alaya_scan", "alaya_attend", "alaya_merge_partials", "alaya_merge_states", "alaya_selected",
+    "alaya_ws_status",
+)
+
+
+class AlayaSeq(ctypes.Structure):
+    """``alaya_seq`` (include/alaya.h)."""
+
+    _fields_ = [
+        ("k", ctypes.c_void_p), ("v", ctypes.c_void_p),
+        ("wk", ctypes.c_void_p), ("wv", ctypes.c_void_p),
+        ("head_stride", ctypes.c_int64), ("w_head_stride", ctypes.c_int64),
+        ("token_offset", ctypes.c_int64), ("prefix_len", ctypes.c_int64),
+        ("n", ctypes.c_int32), ("w", ctypes.c_int32),
+    ]
+
+
+class AlayaParams(ctypes.Structure):
+    """``alaya_params`` (include/alaya.h)."""
+
+    _fields_ = [
+        ("n_query_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32),
+        ("dim", ctypes.c_int32), ("dtype", ctypes.c_int32), ("beta", ctypes.c_float),
+        ("win_initial", ctypes.c_int32), ("win_last", ctypes.c_int32),
+        ("chunk", ctypes.c_int32), ("scan_kind", ctypes.c_int32),
+        ("block_filter", ctypes.c_int32),
+    ]
+
+
+class AlayaError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load the library (no device calls). Raises if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise AlayaError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (or `make -C paper_2504_10326_b200/csrc -j`). There is no CPU fallback.")
+    lib = ctypes.CDLL(str(LIB_PATH), mode=os.RTLD_LOCAL | getattr(os, "RTLD_NOW", 2))
+    P, S = ctypes.POINTER(AlayaParams), ctypes.POINTER(AlayaSeq)
+    vp, i32, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+    lib.alaya_last_error.restype = ctypes.c_char_p
+    lib.alaya_last_error.argtypes = []
+    lib.alaya_version.restype = i32
+    lib.alaya_workspace_bytes.restype = sz
+    lib.alaya_workspace_bytes.argtypes = [P, S, i32]
+    lib.alaya_dipr_attention.restype = i32
+    lib.alaya_dipr_attention.argtypes = [P, S, i32, vp, vp, vp, sz, vp]
+    lib.alaya_scan.restype = i32
+    lib.alaya_scan.argtypes = [P, S, i32, vp, vp, vp, sz, vp]
+    lib.alaya_attend.restype = i32
+    lib.alaya_attend.argtypes = [P, S, i32, vp, vp, vp, i32, vp, sz, vp]
+    lib.alaya_merge_partials.restype = i32
+    lib.alaya_merge_partials.argtypes = [vp, i32, i32, i32, vp, vp, vp]
+    lib.alaya_merge_states.restype = i32
+    lib.alaya_merge_states.argtypes = [vp, i32, i32, i32, vp, vp]
+    lib.alaya_selected.restype = i32
+    lib.alaya_selected.argtypes = [P, S, i32, vp, ctypes.c_int64, vp, vp, vp, sz, vp]
+    lib.alaya_ws_status.restype = vp
+    lib.alaya_ws_status.argtypes = [vp]
+    _lib = lib
+    return lib
+
+
+def check(rc: int) -> None:
+    """Map a C-ABI status to the reference's exception types."""
+    if rc == ALAYA_OK:
+        return
+    msg = load().alaya_last_error().decode(errors="replace")
+    if rc in (ALAYA_ERR_ARG, ALAYA_ERR_SHAPE):
+        raise ValueError(msg)
+    if rc == ALAYA_ERR_NONFINITE:
+        raise FloatingPointError(msg or "attention output is non-finite")
+    if rc == ALAYA_ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise AlayaError(f"alaya status {rc}: {msg}")

@@ -1,0 +1,288 @@
+// C-ABI entry points (include/alaya.h): validation, workspace layout, kernel
+// dispatch over (dtype, dim, group size) and launch.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "alaya_dispatch.cuh"
+#include "alaya_misc_kernels.cuh"
+
+using namespace alaya;
+
+namespace alaya {
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ALAYA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return ALAYA_OK;
+}
+}  // namespace alaya
+
+namespace {
+
+constexpr int kNumSMs = 148;
+
+bool dim_ok(int d) { return d == 16 || d == 32 || d == 64 || d == 128 || d == 256; }
+
+int chunks_for(const alaya_seq* seqs, int B, int Hkv, int chunk) {
+  long total = 0;
+  for (int b = 0; b < B; ++b) total += (long)Hkv * ((seqs[b].n + chunk - 1) / chunk);
+  return (int)total;
+}
+
+// Validate the call and build the kernel-side batch descriptor.
+int build_batch(const alaya_params* p, const alaya_seq* seqs, int B, Batch* bt) {
+  if (!p || !seqs) return fail(ALAYA_ERR_ARG, "null params/seqs");
+  if (B < 1 || B > ALAYA_MAX_BATCH)
+    return fail(ALAYA_ERR_ARG, "batch %d out of range [1, %d]", B, ALAYA_MAX_BATCH);
+  if (p->n_query_heads < 1 || p->n_kv_heads < 1)
+    return fail(ALAYA_ERR_ARG, "all head counts must be positive");
+  if (p->n_query_heads % p->n_kv_heads)
+    return fail(ALAYA_ERR_ARG, "n_query_heads (%d) must be a multiple of n_kv_heads (%d)",
+                p->n_query_heads, p->n_kv_heads);
+  const int G = p->n_query_heads / p->n_kv_heads;
+  if (G > 8) return fail(ALAYA_ERR_UNSUPPORTED, "group size %d > 8", G);
+  if (!dim_ok(p->dim)) return fail(ALAYA_ERR_UNSUPPORTED, "dim %d not in {16,32,64,128,256}", p->dim);
+  if (p->dtype != ALAYA_F32 && p->dtype != ALAYA_BF16) return fail(ALAYA_ERR_ARG, "bad dtype");
+  if (!(p->beta >= 0.f)) return fail(ALAYA_ERR_ARG, "beta must be non-negative, got %g", p->beta);
+  if (p->win_initial < 0 || p->win_last < 0)
+    return fail(ALAYA_ERR_ARG, "window sizes must be non-negative");
+  long tokens = 0;
+  int maxn = 0;
+  for (int b = 0; b < B; ++b) {
+    const alaya_seq& s = seqs[b];
+    if (s.n < 0 || s.w < 0) return fail(ALAYA_ERR_SHAPE, "seq %d: negative row count", b);
+    if (s.n > 0 && (!s.k || !s.v)) return fail(ALAYA_ERR_ARG, "seq %d: null base K/V", b);
+    if (s.w > 0 && (!s.wk || !s.wv)) return fail(ALAYA_ERR_ARG, "seq %d: null window K/V", b);
+    if (s.token_offset < 0 || s.prefix_len < s.token_offset + s.n)
+      return fail(ALAYA_ERR_SHAPE, "seq %d: shard [%lld, +%d) outside prefix %lld", b,
+                  (long long)s.token_offset, s.n, (long long)s.prefix_len);
+    if (s.n > 0 && s.head_stride < (int64_t)s.n * p->dim)
+      return fail(ALAYA_ERR_SHAPE, "seq %d: head_stride too small", b);
+    if (s.w > 0 && s.w_head_stride < (int64_t)s.w * p->dim)
+      return fail(ALAYA_ERR_SHAPE, "seq %d: w_head_stride too small", b);
+    tokens += s.n;
+    if (s.n > maxn) maxn = s.n;
+  }
+  int chunk = p->chunk;
+  if (chunk > 0) {
+    if (chunk % 256 || chunk > 8192) return fail(ALAYA_ERR_ARG, "chunk must be a multiple of 256, <= 8192");
+  } else {
+    chunk = 2048;
+    while (chunk > 256 && chunks_for(seqs, B, p->n_kv_heads, chunk) < 4 * kNumSMs) chunk >>= 1;
+  }
+  if (G * chunk * 4 > 160 * 1024) chunk = ((160 * 1024 / 4 / G) / 256) * 256;
+  (void)tokens;
+  (void)maxn;
+
+  memset(bt, 0, sizeof(Batch));
+  bt->B = B;
+  bt->Hq = p->n_query_heads;
+  bt->Hkv = p->n_kv_heads;
+  bt->G = G;
+  bt->D = p->dim;
+  bt->chunk = chunk;
+  bt->beta = p->beta;
+  bt->wi = p->win_initial;
+  bt->wl = p->win_last;
+  bt->inv_sqrt_d = (float)(1.0 / std::sqrt((double)p->dim));
+  int cb = 0;
+  for (int b = 0; b < B; ++b) {
+    const alaya_seq& s = seqs[b];
+    KSeq& k = bt->s[b];
+    k.k = s.k; k.v = s.v; k.wk = s.wk; k.wv = s.wv;
+    k.hs = s.head_stride; k.whs = s.w_head_stride;
+    k.off = s.token_offset; k.P = s.prefix_len;
+    k.n = s.n; k.w = s.w;
+    k.nch = (s.n + chunk - 1) / chunk;
+    k.chunk_base = cb;
+    cb += p->n_kv_heads * k.nch;
+  }
+  bt->total_chunks = cb;
+  return ALAYA_OK;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Layout {
+  size_t status, gmax, cnt, selcnt, retcnt, part_l, part_acc, cidx, cscore, partbuf, smaxbuf,
+      bfkeep, total;
+};
+
+Layout layout_for(const Batch& bt) {
+  Layout L;
+  const size_t C = (size_t)bt.total_chunks, G = bt.G, D = bt.D, rows = (size_t)bt.B * bt.Hq;
+  size_t o = 0;
+  L.status = o; o = align_up(o + 4);
+  L.gmax = o; o = align_up(o + 4 * rows);
+  L.cnt = o; o = align_up(o + 4 * C * G);
+  L.selcnt = o; o = align_up(o + 4 * C * G);
+  L.retcnt = o; o = align_up(o + 4 * C * G);
+  L.part_l = o; o = align_up(o + 4 * C * G);
+  L.part_acc = o; o = align_up(o + 4 * C * G * D);
+  L.cidx = o; o = align_up(o + 4 * C * G * bt.chunk);
+  L.cscore = o; o = align_up(o + 4 * C * G * bt.chunk);
+  L.partbuf = o; o = align_up(o + 4 * rows * (D + 2));
+  L.smaxbuf = o; o = align_up(o + 4 * rows);
+  L.bfkeep = o; o = align_up(o + 4 * C);
+  L.total = o;
+  return L;
+}
+
+Ws carve(const Layout& L, void* base) {
+  char* c = static_cast<char*>(base);
+  Ws w;
+  w.status = reinterpret_cast<int*>(c + L.status);
+  w.gmax = reinterpret_cast<uint32_t*>(c + L.gmax);
+  w.cnt = reinterpret_cast<int*>(c + L.cnt);
+  w.selcnt = reinterpret_cast<int*>(c + L.selcnt);
+  w.retcnt = reinterpret_cast<int*>(c + L.retcnt);
+  w.part_l = reinterpret_cast<float*>(c + L.part_l);
+  w.part_acc = reinterpret_cast<float*>(c + L.part_acc);
+  w.cidx = reinterpret_cast<int*>(c + L.cidx);
+  w.cscore = reinterpret_cast<float*>(c + L.cscore);
+  w.partbuf = reinterpret_cast<float*>(c + L.partbuf);
+  w.smaxbuf = reinterpret_cast<float*>(c + L.smaxbuf);
+  w.bfkeep = reinterpret_cast<int*>(c + L.bfkeep);
+  return w;
+}
+
+StageSet pick(int dtype, int D, int G) {
+  const bool bf = dtype == ALAYA_BF16;
+  switch (D) {
+    case 16: return bf ? pick_bf16_16(G) : pick_f32_16(G);
+    case 32: return bf ? pick_bf16_32(G) : pick_f32_32(G);
+    case 64: return bf ? pick_bf16_64(G) : pick_f32_64(G);
+    case 128: return bf ? pick_bf16_128(G) : pick_f32_128(G);
+    default: return bf ? pick_bf16_256(G) : pick_f32_256(G);
+  }
+}
+
+struct Call {
+  Batch bt;
+  Layout L;
+  Ws ws;
+  StageSet st;
+  cudaStream_t stream;
+};
+
+int prepare(const alaya_params* p, const alaya_seq* seqs, int B, void* d_ws, size_t ws_bytes,
+            void* stream, Call* c) {
+  int rc = build_batch(p, seqs, B, &c->bt);
+  if (rc) return rc;
+  c->L = layout_for(c->bt);
+  if (!d_ws) return fail(ALAYA_ERR_WORKSPACE, "null workspace");
+  if (ws_bytes < c->L.total)
+    return fail(ALAYA_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, c->L.total);
+  c->ws = carve(c->L, d_ws);
+  c->st = pick(p->dtype, p->dim, c->bt.G);
+  c->stream = static_cast<cudaStream_t>(stream);
+  return ALAYA_OK;
+}
+
+int run_scan(Call& c, const float* d_q) {
+  const size_t rows = (size_t)c.bt.B * c.bt.Hq;
+  if (cudaMemsetAsync(c.ws.gmax, 0, 4 * rows, c.stream) != cudaSuccess) return cuda_check("memset");
+  return c.st.scan(c.bt, d_q, c.ws, c.stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* alaya_last_error(void) { return g_err.c_str(); }
+int alaya_version(void) { return 1; }
+
+size_t alaya_workspace_bytes(const alaya_params* p, const alaya_seq* seqs, int batch) {
+  Batch* bt = new Batch;
+  size_t r = 0;
+  if (build_batch(p, seqs, batch, bt) == ALAYA_OK) r = layout_for(*bt).total;
+  delete bt;
+  return r;
+}
+
+int* alaya_ws_status(void* d_ws) { return static_cast<int*>(d_ws); }
+
+int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q,
+                         float* d_out, void* d_ws, size_t ws_bytes, void* stream) {
+  Call c;
+  int rc = prepare(p, seqs, batch, d_ws, ws_bytes, stream, &c);
+  if (rc) return rc;
+  if (!d_q || !d_out) return fail(ALAYA_ERR_ARG, "null q/out");
+  for (int b = 0; b < batch; ++b)
+    if (seqs[b].prefix_len + seqs[b].w == 0) return fail(ALAYA_ERR_ARG, "attention on an empty session");
+  if (cudaMemsetAsync(c.ws.status, 0, 4, c.stream) != cudaSuccess) return cuda_check("memset");
+  if ((rc = run_scan(c, d_q))) return rc;
+  if ((rc = c.st.attend(c.bt, nullptr, c.ws, 1, c.stream))) return rc;
+  return c.st.combine(c.bt, d_q, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);
+}
+
+int alaya_scan(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q,
+               float* d_smax, void* d_ws, size_t ws_bytes, void* stream) {
+  Call c;
+  int rc = prepare(p, seqs, batch, d_ws, ws_bytes, stream, &c);
+  if (rc) return rc;
+  if (!d_q) return fail(ALAYA_ERR_ARG, "null q");
+  if ((rc = run_scan(c, d_q))) return rc;
+  if (!d_smax) return ALAYA_OK;  // scan only (kernel timing)
+  // export the local max (decoded); combine with no outputs does only that
+  return c.st.combine(c.bt, d_q, nullptr, c.ws, nullptr, nullptr, d_smax, c.stream);
+}
+
+int alaya_attend(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q,
+                 const float* d_smax, float* d_part, int want_values, void* d_ws, size_t ws_bytes,
+                 void* stream) {
+  Call c;
+  int rc = prepare(p, seqs, batch, d_ws, ws_bytes, stream, &c);
+  if (rc) return rc;
+  if (!d_q || !d_smax) return fail(ALAYA_ERR_ARG, "null q/smax");
+  if ((rc = c.st.attend(c.bt, d_smax, c.ws, want_values ? 1 : 0, c.stream))) return rc;
+  if (!want_values || !d_part) return ALAYA_OK;
+  return c.st.combine(c.bt, d_q, d_smax, c.ws, nullptr, d_part, nullptr, c.stream);
+}
+
+int alaya_merge_partials(const float* d_parts, int n_parts, int rows, int dim, float* d_out,
+                         int* d_status, void* stream) {
+  if (!d_parts || !d_out || n_parts < 1 || rows < 0 || !dim_ok(dim))
+    return fail(ALAYA_ERR_ARG, "bad merge arguments");
+  if (rows == 0) return ALAYA_OK;
+  merge_partials_kernel<<<rows, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_parts, n_parts, rows, dim, d_out, nullptr, d_status);
+  return cuda_check("merge_partials_kernel");
+}
+
+int alaya_merge_states(const float* d_parts, int n_parts, int rows, int dim, float* d_state,
+                       void* stream) {
+  if (!d_parts || !d_state || n_parts < 1 || rows < 0 || !dim_ok(dim))
+    return fail(ALAYA_ERR_ARG, "bad merge arguments");
+  if (rows == 0) return ALAYA_OK;
+  merge_partials_kernel<<<rows, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_parts, n_parts, rows, dim, nullptr, d_state, nullptr);
+  return cuda_check("merge_partials_kernel");
+}
+
+int alaya_selected(const alaya_params* p, const alaya_seq* seqs, int batch, int64_t* d_ids,
+                   int64_t cap, int32_t* d_selected, int32_t* d_retrieved, void* d_ws,
+                   size_t ws_bytes, void* stream) {
+  Call c;
+  int rc = prepare(p, seqs, batch, d_ws, ws_bytes, stream, &c);
+  if (rc) return rc;
+  if (!d_ids || !d_selected || !d_retrieved) return fail(ALAYA_ERR_ARG, "null outputs");
+  selected_kernel<<<batch * c.bt.Hq, kThreads, 0, c.stream>>>(c.bt, c.ws, d_ids, cap, d_selected,
+                                                              d_retrieved);
+  return cuda_check("selected_kernel");
+}
+
+}  // extern "C"

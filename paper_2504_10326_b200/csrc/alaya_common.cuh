@@ -1,0 +1,191 @@
+// Shared device helpers and the per-call batch descriptor.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+#include "../../include/alaya.h"
+
+namespace alaya {
+
+constexpr int kThreads = 256;  // every kernel: 8 warps = 16 half-warps
+constexpr int kWarps = kThreads / 32;
+constexpr int kHalfWarps = kThreads / 16;
+constexpr unsigned kFull = 0xffffffffu;
+constexpr float kLog2e = 1.4426950408889634f;
+
+// One sequence of the batch, as the kernels see it (kernel-parameter space).
+struct KSeq {
+  const void* k;
+  const void* v;
+  const void* wk;
+  const void* wv;
+  int64_t hs;    // head stride of k/v (elements)
+  int64_t whs;   // head stride of wk/wv (elements)
+  int64_t off;   // global id of local row 0 (sequence-sharded mode)
+  int64_t P;     // full base-prefix length (window ids are defined on it)
+  int32_t n;     // base rows held here
+  int32_t w;     // session-window rows
+  int32_t chunk_base;  // first work chunk of this sequence
+  int32_t nch;         // chunks per kv head
+};
+
+struct Batch {
+  KSeq s[ALAYA_MAX_BATCH];
+  int32_t B, Hq, Hkv, G, D, chunk;
+  float beta;
+  int32_t wi, wl;
+  int32_t total_chunks;
+  float inv_sqrt_d;
+};
+
+// Workspace pointers (device), carved from the caller's buffer.
+struct Ws {
+  int* status;
+  uint32_t* gmax;   // [B*Hq] order-preserving encoded running max
+  int* cnt;         // [chunks*G] candidate counts
+  int* selcnt;      // [chunks*G]
+  int* retcnt;      // [chunks*G]
+  float* part_l;    // [chunks*G]
+  float* part_acc;  // [chunks*G*D]
+  int* cidx;        // [chunks*G*chunk] candidate local row (then selected, compacted)
+  float* cscore;    // [chunks*G*chunk]
+  float* partbuf;   // [B*Hq*(D+2)]
+  float* smaxbuf;   // [B*Hq]
+  int* bfkeep;      // [chunks] block-filter flags (reserved)
+};
+
+__device__ __forceinline__ uint32_t enc_max(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float dec_max(uint32_t e) {
+  if (e == 0u) return -INFINITY;
+  uint32_t u = (e & 0x80000000u) ? (e & 0x7fffffffu) : ~e;
+  return __uint_as_float(u);
+}
+
+// Work chunk -> (sequence, kv head, chunk within head).
+__device__ __forceinline__ void decode_chunk(const Batch& bt, int c, int& b, int& h, int& ci) {
+  int lo = 0, hi = bt.B - 1;
+  while (lo < hi) {  // last b with chunk_base[b] <= c
+    int mid = (lo + hi + 1) >> 1;
+    if (bt.s[mid].chunk_base <= c) lo = mid; else hi = mid - 1;
+  }
+  b = lo;
+  int local = c - bt.s[b].chunk_base;
+  h = local / bt.s[b].nch;
+  ci = local - h * bt.s[b].nch;
+}
+
+// Window membership of a GLOBAL base id (WindowConfig.base_ids, core.py:159-165).
+__device__ __forceinline__ bool in_window(int64_t gid, int64_t P, int wi, int wl) {
+  if (P <= (int64_t)wi + wl) return true;
+  return gid < wi || gid >= P - wl;
+}
+
+// --- streaming loads -------------------------------------------------------
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint2 ld_stream(const uint2* p) { return __ldg(p); }
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) { return __ldg(p); }
+__device__ __forceinline__ uint16_t ld_stream(const uint16_t* p) {
+  return __ldg(reinterpret_cast<const unsigned short*>(p));
+}
+
+// N elements of T held raw in registers; converted to fp32 on use.
+template <typename T, int N>
+struct RawFrag {
+  static constexpr int BYTES = N * (int)sizeof(T);
+  using V = std::conditional_t<
+      BYTES % 16 == 0, uint4,
+      std::conditional_t<BYTES % 8 == 0, uint2,
+                         std::conditional_t<BYTES % 4 == 0, uint32_t, uint16_t>>>;
+  static constexpr int NV = BYTES / (int)sizeof(V);
+  V v[NV];
+
+  __device__ __forceinline__ void load(const T* p) {
+    const V* q = reinterpret_cast<const V*>(p);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = ld_stream(q + i);
+  }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = V{};
+  }
+  __device__ __forceinline__ uint32_t word(int i) const {  // i-th 32-bit word
+    if constexpr (std::is_same_v<V, uint4>) {
+      const uint4& x = v[i >> 2];
+      int r = i & 3;
+      return r == 0 ? x.x : r == 1 ? x.y : r == 2 ? x.z : x.w;
+    } else if constexpr (std::is_same_v<V, uint2>) {
+      const uint2& x = v[i >> 1];
+      return (i & 1) ? x.y : x.x;
+    } else if constexpr (std::is_same_v<V, uint32_t>) {
+      return v[i];
+    } else {
+      return (uint32_t)v[0];
+    }
+  }
+  __device__ __forceinline__ void to_float(float (&x)[N]) const {
+    if constexpr (std::is_same_v<T, float>) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) x[i] = __uint_as_float(word(i));
+    } else {
+      if constexpr (N == 1) {
+        x[0] = __uint_as_float(word(0) << 16);
+      } else {
+#pragma unroll
+        for (int i = 0; i < N / 2; ++i) {
+          uint32_t u = word(i);
+          x[2 * i] = __uint_as_float(u << 16);
+          x[2 * i + 1] = __uint_as_float(u & 0xffff0000u);
+        }
+      }
+    }
+  }
+};
+
+template <int N>
+__device__ __forceinline__ void load_q(const float* __restrict__ p, float (&x)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) x[i] = __ldg(p + i);
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, m));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(kFull, v, m);
+  return v;
+}
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned r;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
+}
+
+// Deterministic block sum of one float per thread (fixed tree order).
+__device__ __forceinline__ float block_sum(float v, float* red /* >= kWarps */) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < kWarps; ++i) t += red[i];
+  return t;
+}
+
+}  // namespace alaya

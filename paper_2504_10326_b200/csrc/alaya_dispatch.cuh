@@ -1,0 +1,86 @@
+// Host-side launch helpers shared by the C-ABI (alaya.cu) and the kernel
+// instantiation units (inst_*.cu), which are compiled in parallel.
+#pragma once
+
+#include <algorithm>
+#include <string>
+
+#include "alaya_kernels.cuh"
+
+namespace alaya {
+
+int fail(int code, const char* fmt, ...);
+int cuda_check(const char* what);
+
+inline size_t scan_smem(const Batch& bt) {
+  return (size_t)bt.G * bt.chunk * 4 + kWarps * bt.G * 4 + bt.G * 4 + kWarps * bt.G * 4;
+}
+inline size_t attend_smem(const Batch& bt) {
+  size_t wt = std::max((size_t)bt.G * bt.chunk, (size_t)kWarps * bt.G * bt.D) * 4;
+  return wt + bt.chunk / 32 * 4 + bt.chunk * 4 + 2 * kWarps * 4 + kWarps * 4 + 16;
+}
+
+template <typename T, int D, int G>
+struct Stages {
+  static int scan(const Batch& bt, const float* q, const Ws& ws, cudaStream_t st) {
+    if (bt.total_chunks == 0) return ALAYA_OK;
+    size_t sm = scan_smem(bt);
+    cudaFuncSetAttribute(scan_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    scan_kernel<T, D, G><<<bt.total_chunks, kThreads, sm, st>>>(bt, q, ws);
+    return cuda_check("scan_kernel");
+  }
+  static int attend(const Batch& bt, const float* smax, const Ws& ws, int want_values,
+                    cudaStream_t st) {
+    if (bt.total_chunks == 0) return ALAYA_OK;
+    size_t sm = attend_smem(bt);
+    cudaFuncSetAttribute(attend_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attend_kernel<T, D, G><<<bt.total_chunks, kThreads, sm, st>>>(bt, smax, ws, want_values);
+    return cuda_check("attend_kernel");
+  }
+  static int combine(const Batch& bt, const float* q, const float* smax, const Ws& ws, float* out,
+                     float* part_out, float* smax_out, cudaStream_t st) {
+    combine_kernel<T, D, G><<<bt.B * bt.Hkv, kThreads, 0, st>>>(bt, q, smax, ws, out, part_out,
+                                                                smax_out);
+    return cuda_check("combine_kernel");
+  }
+};
+
+using ScanFn = int (*)(const Batch&, const float*, const Ws&, cudaStream_t);
+using AttendFn = int (*)(const Batch&, const float*, const Ws&, int, cudaStream_t);
+using CombineFn = int (*)(const Batch&, const float*, const float*, const Ws&, float*, float*,
+                          float*, cudaStream_t);
+
+struct StageSet {
+  ScanFn scan;
+  AttendFn attend;
+  CombineFn combine;
+};
+
+template <typename T, int D, int G>
+StageSet make_set() {
+  return {&Stages<T, D, G>::scan, &Stages<T, D, G>::attend, &Stages<T, D, G>::combine};
+}
+
+template <typename T, int D>
+StageSet pick_g(int G) {
+  switch (G) {
+    case 1: return make_set<T, D, 1>();
+    case 2: return make_set<T, D, 2>();
+    case 3: return make_set<T, D, 3>();
+    case 4: return make_set<T, D, 4>();
+    case 5: return make_set<T, D, 5>();
+    case 6: return make_set<T, D, 6>();
+    case 7: return make_set<T, D, 7>();
+    default: return make_set<T, D, 8>();
+  }
+}
+
+
+#define ALAYA_DECLARE_PICKS(X)                                                     \
+  X(f32_16) X(f32_32) X(f32_64) X(f32_128) X(f32_256)                              \
+  X(bf16_16) X(bf16_32) X(bf16_64) X(bf16_128) X(bf16_256)
+#define ALAYA_DECL(name) StageSet pick_##name(int G);
+ALAYA_DECLARE_PICKS(ALAYA_DECL)
+#undef ALAYA_DECL
+
+}  // namespace alaya

@@ -1,0 +1,62 @@
+// Non-templated kernels (merge across shards, selected-id export); included
+// only by alaya.cu.
+#pragma once
+
+#include "alaya_common.cuh"
+
+namespace alaya {
+
+// Merge of shard partials (attention.py:128-152), rows = batch * Hq.
+__global__ void merge_partials_kernel(const float* __restrict__ parts, int n_parts, int rows, int D,
+                                      float* __restrict__ out, float* __restrict__ state_out,
+                                      int* status) {
+  const int row = blockIdx.x;
+  const size_t stride = (size_t)rows * (D + 2);
+  float m = -INFINITY;
+  for (int r = 0; r < n_parts; ++r) m = fmaxf(m, parts[r * stride + (size_t)row * (D + 2)]);
+  float l = 0.f;
+  for (int r = 0; r < n_parts; ++r) {
+    const float* p = parts + r * stride + (size_t)row * (D + 2);
+    if (p[0] != -INFINITY) l += p[1] * expf(p[0] - m);
+  }
+  for (int e = threadIdx.x; e < D; e += blockDim.x) {
+    float a = 0.f;
+    for (int r = 0; r < n_parts; ++r) {
+      const float* p = parts + r * stride + (size_t)row * (D + 2);
+      if (p[0] != -INFINITY) a += p[2 + e] * expf(p[0] - m);
+    }
+    if (out) {
+      const float o = a / l;
+      if (!isfinite(o) && status) atomicExch(status, (int)ALAYA_ERR_NONFINITE);
+      out[(size_t)row * D + e] = o;
+    }
+    if (state_out) {
+      float* so = state_out + (size_t)row * (D + 2);
+      if (e == 0) { so[0] = m; so[1] = l; }
+      so[2 + e] = a;
+    }
+  }
+}
+
+// Selected ids (global, ascending) + counts per (sequence, q head).
+__global__ void selected_kernel(const __grid_constant__ Batch bt, Ws ws, int64_t* __restrict__ ids,
+                                int64_t cap, int32_t* __restrict__ nsel, int32_t* __restrict__ nret) {
+  const int row = blockIdx.x;  // b*Hq + qh
+  const int b = row / bt.Hq, qh = row - b * bt.Hq;
+  const int h = qh / bt.G, j = qh - h * bt.G;
+  const KSeq& s = bt.s[b];
+  const int c0 = s.chunk_base + h * s.nch;
+  int base = 0, ret = 0;
+  for (int c = 0; c < s.nch; ++c) {
+    const size_t cj = (size_t)(c0 + c) * bt.G + j;
+    const int n = ws.selcnt[cj];
+    const int* src = ws.cidx + cj * bt.chunk;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      if (base + i < cap) ids[(size_t)row * cap + base + i] = s.off + (int64_t)c * bt.chunk + src[i];
+    base += n;
+    ret += ws.retcnt[cj];
+  }
+  if (threadIdx.x == 0) { nsel[row] = base; nret[row] = ret; }
+}
+
+}  // namespace alaya

@@ -1,0 +1,6 @@
+// Kernel instantiations for dtype=bf16, dim=256, group sizes 1..8.
+#include "alaya_dispatch.cuh"
+
+namespace alaya {
+StageSet pick_bf16_256(int G) { return pick_g<__nv_bfloat16, 256>(G); }
+}  // namespace alaya

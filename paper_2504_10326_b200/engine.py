@@ -1,0 +1,233 @@
+"""Device-side engine: torch tensors in, C-ABI calls out.
+
+PyTorch is plumbing here (device memory, streams, collectives); every
+arithmetic step of the hot path runs in ``libalaya_b200.so``. The stages map
+onto the reference's flat decode step (``store.py:252-293``):
+
+=====================  =================================================
+``scan``               scores + per-head max + candidate superset
+``attend``             exact ``>= max - beta`` filter, window exclusion,
+                       V gather, online softmax -> (m, l, acc) per head
+``merge_partials``     ``PartialAttention.merge`` + ``finalize``
+``dipr_attention``     all three in one stream-ordered call
+``selected``           the critical id sets (``dipr_bruteforce`` output)
+=====================  =================================================
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import AlayaParams, AlayaSeq, check
+
+_DTYPES = {torch.float32: _lib.ALAYA_F32, torch.bfloat16: _lib.ALAYA_BF16}
+
+
+def require_cuda() -> None:
+    """Fail loudly: the product path has no CPU fallback."""
+    _lib.load()
+    if not torch.cuda.is_available():
+        raise _lib.AlayaError("no CUDA device: the alaya B200 path has no CPU fallback")
+
+
+@dataclass
+class SeqView:
+    """One sequence (session) at one layer, as device tensors.
+
+    ``k``/``v``: ``[Hkv, rows >= n, d]`` base prefix (row stride must be d);
+    ``wk``/``wv``: ``[Hkv, rows >= w, d]`` session-window rows or None.
+    ``token_offset``/``prefix_len`` describe a sequence shard.
+    """
+
+    k: torch.Tensor | None
+    v: torch.Tensor | None
+    n: int
+    wk: torch.Tensor | None = None
+    wv: torch.Tensor | None = None
+    w: int = 0
+    token_offset: int = 0
+    prefix_len: int | None = None
+
+
+def _check_kv(t: torch.Tensor, name: str, dtype, d: int) -> None:
+    if t.dtype != dtype:
+        raise ValueError(f"{name} dtype {t.dtype} != {dtype}")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dim() != 3 or t.shape[2] != d or t.stride(2) != 1 or t.stride(1) != d:
+        raise ValueError(f"{name} must be [heads, rows, {d}] with unit row stride, got "
+                         f"{tuple(t.shape)} strides {t.stride()}")
+
+
+def make_params(n_query_heads: int, n_kv_heads: int, dim: int, dtype: torch.dtype, beta: float,
+                win_initial: int, win_last: int, chunk: int = 0, scan_kind: int = 0,
+                block_filter: int = 0) -> AlayaParams:
+    if dtype not in _DTYPES:
+        raise ValueError(f"unsupported KV dtype {dtype}")
+    if beta < 0:
+        raise ValueError(f"beta must be non-negative, got {beta}")
+    return AlayaParams(n_query_heads, n_kv_heads, dim, _DTYPES[dtype], float(beta),
+                       int(win_initial), int(win_last), int(chunk), int(scan_kind),
+                       int(block_filter))
+
+
+def seq_array(seqs: list[SeqView], params: AlayaParams, dtype: torch.dtype):
+    d = params.dim
+    arr = (AlayaSeq * len(seqs))()
+    for i, s in enumerate(seqs):
+        e = arr[i]
+        if s.n:
+            _check_kv(s.k, "k", dtype, d)
+            _check_kv(s.v, "v", dtype, d)
+            if s.k.shape[0] != params.n_kv_heads or s.k.shape[1] < s.n:
+                raise ValueError(f"base K shape {tuple(s.k.shape)} vs n={s.n}")
+            if s.v.stride(0) != s.k.stride(0):
+                raise ValueError("k and v must share a head stride")
+            e.k, e.v, e.head_stride = s.k.data_ptr(), s.v.data_ptr(), s.k.stride(0)
+        if s.w:
+            _check_kv(s.wk, "wk", dtype, d)
+            _check_kv(s.wv, "wv", dtype, d)
+            if s.wk.shape[1] < s.w or s.wv.stride(0) != s.wk.stride(0):
+                raise ValueError("window K/V shape mismatch")
+            e.wk, e.wv, e.w_head_stride = s.wk.data_ptr(), s.wv.data_ptr(), s.wk.stride(0)
+        e.n, e.w = int(s.n), int(s.w)
+        e.token_offset = int(s.token_offset)
+        e.prefix_len = int(s.n + s.token_offset if s.prefix_len is None else s.prefix_len)
+    return arr
+
+
+class _Workspace(threading.local):
+    def __init__(self):
+        self.buf: dict[int, torch.Tensor] = {}
+
+    def get(self, nbytes: int, device: torch.device) -> torch.Tensor:
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+        t = self.buf.get(idx)
+        if t is None or t.numel() < nbytes:
+            t = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+            self.buf[idx] = t
+        return t
+
+
+_WS = _Workspace()
+
+
+class Call:
+    """One validated batch: params + descriptors + workspace (reused by stages)."""
+
+    def __init__(self, seqs: list[SeqView], params: AlayaParams, dtype: torch.dtype,
+                 device: torch.device, ws: torch.Tensor | None = None):
+        require_cuda()
+        self.lib = _lib.load()
+        if not 1 <= len(seqs) <= _lib.MAX_BATCH:
+            raise ValueError(f"batch must be in [1, {_lib.MAX_BATCH}]")
+        self.params = params
+        self.seqs = seq_array(seqs, params, dtype)
+        self.B = len(seqs)
+        self.device = device
+        nbytes = self.lib.alaya_workspace_bytes(ctypes.byref(params), self.seqs, self.B)
+        if nbytes == 0:
+            check(_lib.ALAYA_ERR_ARG)
+        self.ws = ws if ws is not None and ws.numel() >= nbytes else _WS.get(nbytes, device)
+        self.ws_bytes = self.ws.numel()
+
+    @property
+    def stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def _q(self, q: torch.Tensor) -> torch.Tensor:
+        p = self.params
+        if q.shape != (self.B, p.n_query_heads, p.dim):
+            raise ValueError(f"q must be {(self.B, p.n_query_heads, p.dim)}, got {tuple(q.shape)}")
+        return q.to(device=self.device, dtype=torch.float32).contiguous()
+
+    def dipr_attention(self, q: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        q = self._q(q)
+        if out is None:
+            out = torch.empty_like(q)
+        check(self.lib.alaya_dipr_attention(ctypes.byref(self.params), self.seqs, self.B,
+                                            q.data_ptr(), out.data_ptr(), self.ws.data_ptr(),
+                                            self.ws_bytes, self.stream))
+        self._q_keep = q
+        return out
+
+    def set_window_rows(self, w: int) -> None:
+        """Update every sequence's session-window row count (fast per-step rebind;
+        the caller guarantees the window tensors hold >= w rows)."""
+        for i in range(self.B):
+            self.seqs[i].w = int(w)
+
+    def scan_only(self, q: torch.Tensor) -> None:
+        """Stage 1 alone (no max export): used to time the scan kernel."""
+        check(self.lib.alaya_scan(ctypes.byref(self.params), self.seqs, self.B, q.data_ptr(),
+                                  None, self.ws.data_ptr(), self.ws_bytes, self.stream))
+
+    def status(self) -> int:
+        """Device status word of the last dipr_attention (synchronises)."""
+        return int(self.ws[:4].view(torch.int32).item())
+
+    def scan(self, q: torch.Tensor) -> torch.Tensor:
+        q = self._q(q)
+        smax = torch.empty(self.B, self.params.n_query_heads, dtype=torch.float32,
+                           device=self.device)
+        check(self.lib.alaya_scan(ctypes.byref(self.params), self.seqs, self.B, q.data_ptr(),
+                                  smax.data_ptr(), self.ws.data_ptr(), self.ws_bytes,
+                                  self.stream))
+        self._q_keep = q
+        return smax
+
+    def attend(self, q: torch.Tensor, smax: torch.Tensor, want_values: bool = True):
+        q = self._q(q)
+        smax = smax.to(device=self.device, dtype=torch.float32).contiguous()
+        part = None
+        if want_values:
+            part = torch.empty(self.B * self.params.n_query_heads, self.params.dim + 2,
+                               dtype=torch.float32, device=self.device)
+        check(self.lib.alaya_attend(ctypes.byref(self.params), self.seqs, self.B, q.data_ptr(),
+                                    smax.data_ptr(), part.data_ptr() if part is not None else None,
+                                    int(want_values), self.ws.data_ptr(), self.ws_bytes,
+                                    self.stream))
+        self._q_keep = q
+        return part
+
+    def selected(self, cap: int):
+        """Per (seq, q head) selected ids (ascending, global) + counts; after attend/attention."""
+        rows = self.B * self.params.n_query_heads
+        ids = torch.empty(rows, max(cap, 1), dtype=torch.int64, device=self.device)
+        nsel = torch.empty(rows, dtype=torch.int32, device=self.device)
+        nret = torch.empty(rows, dtype=torch.int32, device=self.device)
+        check(self.lib.alaya_selected(ctypes.byref(self.params), self.seqs, self.B, ids.data_ptr(),
+                                      ids.shape[1], nsel.data_ptr(), nret.data_ptr(),
+                                      self.ws.data_ptr(), self.ws_bytes, self.stream))
+        return ids, nsel, nret
+
+
+def merge_partials(parts: torch.Tensor, dim: int, status: torch.Tensor | None = None
+                   ) -> torch.Tensor:
+    """Merge ``parts [R, rows, dim+2]`` in order and finalize -> ``[rows, dim]``."""
+    require_cuda()
+    lib = _lib.load()
+    parts = parts.to(torch.float32).contiguous()
+    R, rows = parts.shape[0], parts.shape[1]
+    out = torch.empty(rows, dim, dtype=torch.float32, device=parts.device)
+    check(lib.alaya_merge_partials(parts.data_ptr(), R, rows, dim, out.data_ptr(),
+                                   status.data_ptr() if status is not None else None,
+                                   torch.cuda.current_stream(parts.device).cuda_stream))
+    return out
+
+
+def merge_states(parts: torch.Tensor, dim: int) -> torch.Tensor:
+    """Merge ``parts [R, rows, dim+2]`` in order -> state ``[rows, dim+2]`` (no finalize)."""
+    require_cuda()
+    lib = _lib.load()
+    parts = parts.to(torch.float32).contiguous()
+    R, rows = parts.shape[0], parts.shape[1]
+    out = torch.empty(rows, dim + 2, dtype=torch.float32, device=parts.device)
+    check(lib.alaya_merge_states(parts.data_ptr(), R, rows, dim, out.data_ptr(),
+                                 torch.cuda.current_stream(parts.device).cuda_stream))
+    return out

@@ -1,0 +1,368 @@
+"""Context store and sessions (reference ``sparsekv/store.py``), GPU-resident.
+
+The store owns each imported context's K/V as device tensors
+``[L, Hkv, n, d]`` (fp32 like the reference, or bf16); a session owns a
+device window ring ``[L, Hkv, cap, d]`` that ``update`` appends to (late
+materialization: the base context is never written, ``store.py:160-189``).
+``Session.attention`` issues ONE C-ABI call per layer for all query heads
+(the reference loops heads in Python, ``store.py:209``);
+``attention_batch`` does the same for many sessions at once.
+
+Out of scope (host lifecycle, not the decode step): AVDB persistence
+(``root=``), graph/coarse index construction, TOP_K plans.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib, engine
+from .config import EngineConfig
+from .core import ModelShape, WindowConfig
+from .planner import IndexKind, Plan, PlanRequest, QueryKind, plan as make_plan
+
+_TORCH_DTYPE = {"float32": torch.float32, "bfloat16": torch.bfloat16}
+_SCAN_KIND = {"auto": _lib.SCAN_AUTO, "cuda_core": _lib.SCAN_CUDA_CORE,
+              "tcgen05": _lib.SCAN_TCGEN05}
+
+
+def context_id_for(token_ids: np.ndarray, shape: ModelShape) -> str:
+    """Content-derived id, same bytes hashed as the reference (``store.py:43-48``)."""
+    h = hashlib.sha256()
+    h.update(np.asarray(token_ids, dtype=np.int64).tobytes())
+    h.update(f"{shape.n_layers}/{shape.n_kv_heads}/{shape.dim}".encode())
+    return "ctx-" + h.hexdigest()[:16]
+
+
+def _to_device(x, device, dtype) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        return x.to(device=device, dtype=dtype).contiguous()
+    a = np.asarray(x, dtype=np.float32)
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device=device, dtype=dtype)
+
+
+@dataclass
+class ContextRecord:
+    """Imported context: prompt ids, device K/V ``[L, Hkv, n, d]``, plans."""
+
+    context_id: str
+    token_ids: np.ndarray
+    keys: torch.Tensor
+    values: torch.Tensor
+    shape: ModelShape
+    plans: dict[int, Plan]
+    indexes: dict = field(default_factory=dict)
+
+    @property
+    def length(self) -> int:
+        return int(self.token_ids.shape[0])
+
+    def check_invariants(self) -> None:
+        expect = (self.shape.n_layers, self.shape.n_kv_heads, self.length, self.shape.dim)
+        if tuple(self.keys.shape) != expect or tuple(self.values.shape) != expect:
+            raise AssertionError(f"K/V shape {tuple(self.keys.shape)} != {expect}")
+
+
+@dataclass
+class TwoSegmentView:
+    """Logical K or V of one kv head: base prefix + session window (``store.py:77-93``)."""
+
+    base: torch.Tensor
+    extra: torch.Tensor
+
+    def __len__(self) -> int:
+        return self.base.shape[0] + self.extra.shape[0]
+
+    def materialize(self) -> torch.Tensor:
+        return torch.cat([self.base, self.extra]) if self.extra.shape[0] else self.base
+
+
+class Session:
+    """Reused prefix + growing window; one logical request (``store.py:96-101``)."""
+
+    def __init__(self, store: "ContextStore", base: ContextRecord | None, reused_prefix_len: int):
+        self._store = store
+        self.base = base
+        self.reused_prefix_len = reused_prefix_len
+        shape = store.shape
+        self._wlen = [0] * shape.n_layers
+        self._wk: torch.Tensor | None = None
+        self._wv: torch.Tensor | None = None
+        self._query_log: list[list[np.ndarray]] = [[] for _ in range(shape.n_layers)]
+        self.generated_token_ids: list[int] = []
+        self.plan_override: Plan | dict[int, Plan] | None = None
+        self._diag = None
+
+    # -- state ------------------------------------------------------------
+    @property
+    def window_len(self) -> int:
+        return self._wlen[0]
+
+    @property
+    def total_len(self) -> int:
+        return self.reused_prefix_len + self.window_len
+
+    def record_token(self, token_id: int) -> None:
+        self.generated_token_ids.append(int(token_id))
+
+    def window_arrays(self, layer: int, kv_head: int):
+        w = self._wlen[layer]
+        d = self._store.shape.dim
+        if w == 0:
+            e = np.empty((0, d), dtype=np.float32)
+            return e, e
+        return (self._wk[layer, kv_head, :w].float().cpu().numpy(),
+                self._wv[layer, kv_head, :w].float().cpu().numpy())
+
+    def logged_queries(self, layer: int) -> list[np.ndarray]:
+        shape = self._store.shape
+        rows = self._query_log[layer]
+        if not rows:
+            return [np.empty((0, shape.dim), np.float32) for _ in range(shape.n_query_heads)]
+        q = np.stack(rows)
+        return [q[:, qh] for qh in range(shape.n_query_heads)]
+
+    def _ensure_window(self, need: int) -> None:
+        st = self._store
+        cap = 0 if self._wk is None else self._wk.shape[2]
+        if need <= cap:
+            return
+        new_cap = max(64, cap * 2, need)
+        sh = (st.shape.n_layers, st.shape.n_kv_heads, new_cap, st.shape.dim)
+        wk = torch.zeros(sh, dtype=st.kv_dtype, device=st.device)
+        wv = torch.zeros(sh, dtype=st.kv_dtype, device=st.device)
+        if self._wk is not None:
+            wk[:, :, :cap] = self._wk
+            wv[:, :, :cap] = self._wv
+        self._wk, self._wv = wk, wv
+
+    # -- Table-3 APIs -----------------------------------------------------
+    def update(self, q, k, v, layer: int):
+        """Append one step's per-head K/V to the layer window (``store.py:160-189``)."""
+        st = self._store
+        shape = st.shape
+        self._check_layer(layer)
+        qa = q if isinstance(q, torch.Tensor) else np.atleast_2d(np.asarray(q, dtype=np.float32))
+        if tuple(qa.shape) != (shape.n_query_heads, shape.dim):
+            raise ValueError(f"q must be {(shape.n_query_heads, shape.dim)}, got {tuple(qa.shape)}")
+        kt = k if isinstance(k, torch.Tensor) else np.atleast_2d(np.asarray(k, dtype=np.float32))
+        vt = v if isinstance(v, torch.Tensor) else np.atleast_2d(np.asarray(v, dtype=np.float32))
+        if tuple(kt.shape) != (shape.n_kv_heads, shape.dim) or tuple(vt.shape) != tuple(kt.shape):
+            raise ValueError(f"k/v must be {(shape.n_kv_heads, shape.dim)}")
+        w = self._wlen[layer]
+        self._ensure_window(w + 1)
+        self._wk[layer, :, w] = _to_device(kt, st.device, st.kv_dtype)
+        self._wv[layer, :, w] = _to_device(vt, st.device, st.kv_dtype)
+        self._wlen[layer] = w + 1
+        if st.log_queries:
+            self._query_log[layer].append(
+                qa.detach().float().cpu().numpy() if isinstance(qa, torch.Tensor) else qa.copy())
+        k_views, v_views = [], []
+        for h in range(shape.n_kv_heads):
+            bk, bv = self._base_arrays(layer, h)
+            k_views.append(TwoSegmentView(bk, self._wk[layer, h, : w + 1]))
+            v_views.append(TwoSegmentView(bv, self._wv[layer, h, : w + 1]))
+        return k_views, v_views
+
+    def attention(self, q, layer: int):
+        """Sparse attention outputs for one layer, one row per query head
+        (``store.py:191-216``). numpy in -> numpy out (synchronises and raises
+        ``FloatingPointError`` on non-finite output); CUDA tensor in -> CUDA
+        tensor out, stream-ordered."""
+        if isinstance(q, torch.Tensor):
+            return Session.attention_batch([self], q.unsqueeze(0), layer)[0]
+        return Session.attention_batch([self], np.asarray(q, dtype=np.float32)[None], layer)[0]
+
+    @staticmethod
+    def attention_batch(sessions: list["Session"], q, layer: int):
+        """One decode step of ``layer`` for many sessions of the same store in
+        one kernel sequence. ``q`` is ``[B, Hq, d]`` (numpy or CUDA tensor)."""
+        if not sessions:
+            raise ValueError("empty session batch")
+        st = sessions[0]._store
+        shape = st.shape
+        as_numpy = not isinstance(q, torch.Tensor)
+        qt = torch.from_numpy(np.ascontiguousarray(q, dtype=np.float32)) if as_numpy else q
+        if tuple(qt.shape[1:]) != (shape.n_query_heads, shape.dim) or qt.shape[0] != len(sessions):
+            want = (shape.n_query_heads, shape.dim)
+            raise ValueError(f"q must be {want}, got {tuple(qt.shape[1:])}")
+        groups: dict[tuple, list[int]] = {}
+        for i, s in enumerate(sessions):
+            if s._store is not st:
+                raise ValueError("all sessions of a batch must share a store")
+            s._check_layer(layer)
+            if s.total_len == 0:
+                raise ValueError("attention on an empty session")
+            active = s.active_plan(layer)
+            beta, wi, wl = s._exec_params(active)
+            groups.setdefault((beta, wi, wl), []).append(i)
+        qd = qt.to(device=st.device, dtype=torch.float32, non_blocking=True)
+        out = torch.empty(len(sessions), shape.n_query_heads, shape.dim, dtype=torch.float32,
+                          device=st.device)
+        calls = []
+        for (beta, wi, wl), idx in groups.items():
+            for c0 in range(0, len(idx), _lib.MAX_BATCH):
+                part = idx[c0:c0 + _lib.MAX_BATCH]
+                seqs = [sessions[i]._seq_view(layer) for i in part]
+                params = engine.make_params(shape.n_query_heads, shape.n_kv_heads, shape.dim,
+                                            st.kv_dtype, beta, wi, wl, st.config.chunk,
+                                            _SCAN_KIND[st.config.scan_kernel],
+                                            int(st.config.block_filter))
+                call = engine.Call(seqs, params, st.kv_dtype, st.device)
+                sel = torch.tensor(part, device=st.device) if len(part) != len(sessions) else None
+                o = call.dipr_attention(qd if sel is None else qd.index_select(0, sel))
+                if sel is None:
+                    out = o
+                else:
+                    out.index_copy_(0, sel, o)
+                if st.config.diagnostics:
+                    cap = max(1, max(sv.n for sv in seqs))
+                    ids, nsel, nret = call.selected(cap)
+                    hq = shape.n_query_heads
+                    for j, i in enumerate(part):
+                        s = sessions[i]
+                        r = slice(j * hq, (j + 1) * hq)
+                        s._diag = (layer, s.active_plan(layer), ids[r], nsel[r], nret[r],
+                                   s.reused_prefix_len if s.base is not None else 0, wi, wl)
+                calls.append(call)
+        if as_numpy:
+            res = out.cpu().numpy()
+            if any(c.status() != 0 for c in calls) or not np.isfinite(res).all():
+                raise FloatingPointError("partial attention finalized to non-finite output")
+            return res
+        return out
+
+    @property
+    def last_diagnostics(self) -> dict:
+        """``{layer, plan, heads[{query_head, selected_base, window_base, retrieved}]}``
+        (``store.py:213-215,288-292``), materialised on access."""
+        if self._diag is None:
+            return {}
+        layer, active, ids, nsel, nret, p, wi, wl = self._diag
+        ids, nsel, nret = ids.cpu().numpy(), nsel.cpu().numpy(), nret.cpu().numpy()
+        window = WindowConfig(wi, wl).base_ids(p).tolist()
+        heads = []
+        for qh in range(ids.shape[0]):
+            if active.query is QueryKind.FULL_ATTENTION:
+                info = {"selected_base": list(range(p)), "window_base": window, "retrieved": p}
+            else:
+                info = {"selected_base": ids[qh, : nsel[qh]].tolist(), "window_base": window,
+                        "retrieved": int(nret[qh])}
+            info["query_head"] = qh
+            heads.append(info)
+        return {"layer": layer, "plan": active, "heads": heads}
+
+    # -- internals ----------------------------------------------------------
+    def _check_layer(self, layer: int) -> None:
+        if not 0 <= layer < self._store.shape.n_layers:
+            raise ValueError(f"layer {layer} out of range")
+
+    def _base_arrays(self, layer: int, head: int):
+        p = self.reused_prefix_len
+        st = self._store
+        if self.base is None or p == 0:
+            e = torch.empty(0, st.shape.dim, dtype=st.kv_dtype, device=st.device)
+            return e, e
+        return self.base.keys[layer, head, :p], self.base.values[layer, head, :p]
+
+    def _seq_view(self, layer: int) -> engine.SeqView:
+        p = self.reused_prefix_len if self.base is not None else 0
+        w = self._wlen[layer]
+        return engine.SeqView(
+            k=self.base.keys[layer] if p else None, v=self.base.values[layer] if p else None, n=p,
+            wk=self._wk[layer] if w else None, wv=self._wv[layer] if w else None, w=w)
+
+    def _exec_params(self, active: Plan):
+        """(beta, window initial, window last) the kernels run for a plan."""
+        cfg = self._store.config
+        if active.query is QueryKind.FULL_ATTENTION:
+            return math.inf, 0, 0  # every base token selected, no window split
+        if active.query is QueryKind.TOP_K:
+            raise NotImplementedError("TOP_K / coarse plans are not implemented on the B200 engine")
+        beta = active.beta if active.beta is not None else cfg.beta
+        return float(beta), cfg.window_initial, cfg.window_last
+
+    def active_plan(self, layer: int) -> Plan:
+        """Override (global or per layer) else planned (``store.py:231-250``)."""
+        if isinstance(self.plan_override, dict):
+            if layer in self.plan_override:
+                return self.plan_override[layer]
+        elif self.plan_override is not None:
+            return self.plan_override
+        partial = (self.base is not None and 0 < self.reused_prefix_len < self.base.length
+                   and self.reused_prefix_len < self.total_len)
+        req = PlanRequest(context_len=self.total_len, layer=layer, shape=self._store.shape,
+                          memory_budget_bytes=self._store.config.memory_budget_bytes,
+                          reused_prefix_len=self.reused_prefix_len if partial else None)
+        return make_plan(req, self._store.config.planner_config())
+
+    def full_kv(self, layer: int, head: int):
+        bk, bv = self._base_arrays(layer, head)
+        w = self._wlen[layer]
+        if w == 0:
+            return bk, bv
+        return (torch.cat([bk, self._wk[layer, head, :w]]), torch.cat([bv, self._wv[layer, head, :w]]))
+
+
+class ContextStore:
+    """The "DB" of imported contexts, resident in HBM (``store.py:363-422``)."""
+
+    def __init__(self, shape: ModelShape, config: EngineConfig | None = None, root=None,
+                 pool=None, device=None, log_queries: bool = True):
+        if root is not None or pool is not None:
+            raise NotImplementedError("AVDB persistence / buffer pool are out of scope")
+        engine.require_cuda()
+        self.shape = shape
+        self.config = config or EngineConfig()
+        self.device = torch.device(device or "cuda")
+        self.kv_dtype = _TORCH_DTYPE[self.config.kv_dtype]
+        self.log_queries = log_queries
+        self.contexts: dict[str, ContextRecord] = {}
+
+    def import_context(self, token_ids, keys, values, queries=None) -> str:
+        """Import K/V ``[L, Hkv, n, d]`` (numpy or torch) to the device (``store.py:388-422``)."""
+        token_ids = np.asarray(token_ids, dtype=np.int64)
+        cid = context_id_for(token_ids, self.shape)
+        if cid in self.contexts:
+            return cid
+        n = token_ids.shape[0]
+        expect = (self.shape.n_layers, self.shape.n_kv_heads, n, self.shape.dim)
+        if tuple(keys.shape) != expect or tuple(values.shape) != expect:
+            raise ValueError(f"K/V must have shape {expect}, got {tuple(keys.shape)}")
+        kd = _to_device(keys, self.device, self.kv_dtype)
+        vd = _to_device(values, self.device, self.kv_dtype)
+        if not (torch.isfinite(kd).all() and torch.isfinite(vd).all()):
+            raise ValueError("matrix contains non-finite elements")
+        record = ContextRecord(cid, token_ids, kd, vd, self.shape, self._plans_for(n))
+        record.indexes = {(l, h): IndexKind.FLAT for l in range(self.shape.n_layers)
+                          for h in range(self.shape.n_kv_heads)}
+        record.check_invariants()
+        self.contexts[cid] = record
+        return cid
+
+    def create_session(self, token_ids):
+        """Longest-common-prefix reuse, ties to the latest (``store.py:424-438``)."""
+        token_ids = np.asarray(token_ids, dtype=np.int64)
+        best, best_len = None, 0
+        for record in self.contexts.values():
+            m = min(token_ids.shape[0], record.token_ids.shape[0])
+            neq = np.flatnonzero(token_ids[:m] != record.token_ids[:m])
+            lcp = int(neq[0]) if neq.size else m
+            if lcp >= best_len and lcp > 0:
+                best, best_len = record, lcp
+        return Session(self, best, best_len), token_ids[best_len:].tolist()
+
+    def get(self, context_id: str) -> ContextRecord:
+        return self.contexts[context_id]
+
+    def _plans_for(self, n: int) -> dict[int, Plan]:
+        cfg = self.config.planner_config()
+        return {layer: make_plan(PlanRequest(context_len=n, layer=layer, shape=self.shape,
+                                             memory_budget_bytes=self.config.memory_budget_bytes),
+                                 cfg)
+                for layer in range(self.shape.n_layers)}
