@@ -172,6 +172,8 @@ StageSet pick(int dtype, int D, int G) {
 
 struct Call {
   Batch bt;
+  const alaya_seq* seqs;
+  bool use_tc;
   Layout L;
   Ws ws;
   StageSet st;
@@ -188,6 +190,12 @@ int prepare(const alaya_params* p, const alaya_seq* seqs, int B, void* d_ws, siz
     return fail(ALAYA_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, c->L.total);
   c->ws = carve(c->L, d_ws);
   c->st = pick(p->dtype, p->dim, c->bt.G);
+  c->seqs = seqs;
+  const bool eligible = tc_scan_eligible(c->bt, p->dtype, seqs);
+  if (p->scan_kind == ALAYA_SCAN_TCGEN05 && !eligible)
+    return fail(ALAYA_ERR_UNSUPPORTED, "tcgen05 scan needs bf16 K, dim 128, group <= 8, "
+                "16-byte aligned slabs with a head stride multiple of 128");
+  c->use_tc = eligible && p->scan_kind != ALAYA_SCAN_CUDA_CORE;
   c->stream = static_cast<cudaStream_t>(stream);
   return ALAYA_OK;
 }
@@ -195,6 +203,7 @@ int prepare(const alaya_params* p, const alaya_seq* seqs, int B, void* d_ws, siz
 int run_scan(Call& c, const float* d_q) {
   const size_t rows = (size_t)c.bt.B * c.bt.Hq;
   if (cudaMemsetAsync(c.ws.gmax, 0, 4 * rows, c.stream) != cudaSuccess) return cuda_check("memset");
+  if (c.use_tc) return launch_tc_scan(c.bt, c.seqs, d_q, c.ws, c.stream);
   return c.st.scan(c.bt, d_q, c.ws, c.stream);
 }
 
@@ -225,8 +234,8 @@ int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch
     if (seqs[b].prefix_len + seqs[b].w == 0) return fail(ALAYA_ERR_ARG, "attention on an empty session");
   if (cudaMemsetAsync(c.ws.status, 0, 4, c.stream) != cudaSuccess) return cuda_check("memset");
   if ((rc = run_scan(c, d_q))) return rc;
-  if ((rc = c.st.attend(c.bt, nullptr, c.ws, 1, c.stream))) return rc;
-  return c.st.combine(c.bt, d_q, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);
+  if ((rc = c.st.attend(c.bt, d_q, nullptr, c.ws, 1, c.stream))) return rc;
+  return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);
 }
 
 int alaya_scan(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q,
@@ -238,7 +247,7 @@ int alaya_scan(const alaya_params* p, const alaya_seq* seqs, int batch, const fl
   if ((rc = run_scan(c, d_q))) return rc;
   if (!d_smax) return ALAYA_OK;  // scan only (kernel timing)
   // export the local max (decoded); combine with no outputs does only that
-  return c.st.combine(c.bt, d_q, nullptr, c.ws, nullptr, nullptr, d_smax, c.stream);
+  return c.st.combine(c.bt, nullptr, c.ws, nullptr, nullptr, d_smax, c.stream);
 }
 
 int alaya_attend(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q,
@@ -248,9 +257,9 @@ int alaya_attend(const alaya_params* p, const alaya_seq* seqs, int batch, const 
   int rc = prepare(p, seqs, batch, d_ws, ws_bytes, stream, &c);
   if (rc) return rc;
   if (!d_q || !d_smax) return fail(ALAYA_ERR_ARG, "null q/smax");
-  if ((rc = c.st.attend(c.bt, d_smax, c.ws, want_values ? 1 : 0, c.stream))) return rc;
+  if ((rc = c.st.attend(c.bt, d_q, d_smax, c.ws, want_values ? 1 : 0, c.stream))) return rc;
   if (!want_values || !d_part) return ALAYA_OK;
-  return c.st.combine(c.bt, d_q, d_smax, c.ws, nullptr, d_part, nullptr, c.stream);
+  return c.st.combine(c.bt, d_smax, c.ws, nullptr, d_part, nullptr, c.stream);
 }
 
 int alaya_merge_partials(const float* d_parts, int n_parts, int rows, int dim, float* d_out,

@@ -15,10 +15,6 @@ int cuda_check(const char* what);
 inline size_t scan_smem(const Batch& bt) {
   return (size_t)bt.G * bt.chunk * 4 + kWarps * bt.G * 4 + bt.G * 4 + kWarps * bt.G * 4;
 }
-inline size_t attend_smem(const Batch& bt) {
-  size_t wt = std::max((size_t)bt.G * bt.chunk, (size_t)kWarps * bt.G * bt.D) * 4;
-  return wt + bt.chunk / 32 * 4 + bt.chunk * 4 + 2 * kWarps * 4 + kWarps * 4 + 16;
-}
 
 template <typename T, int D, int G>
 struct Stages {
@@ -29,26 +25,26 @@ struct Stages {
     scan_kernel<T, D, G><<<bt.total_chunks, kThreads, sm, st>>>(bt, q, ws);
     return cuda_check("scan_kernel");
   }
-  static int attend(const Batch& bt, const float* smax, const Ws& ws, int want_values,
-                    cudaStream_t st) {
-    if (bt.total_chunks == 0) return ALAYA_OK;
-    size_t sm = attend_smem(bt);
-    cudaFuncSetAttribute(attend_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attend_kernel<T, D, G><<<bt.total_chunks, kThreads, sm, st>>>(bt, smax, ws, want_values);
+  static int attend(const Batch& bt, const float* q, const float* smax, const Ws& ws,
+                    int want_values, cudaStream_t st) {
+    const long tasks = (long)bt.total_chunks * G + (want_values ? (long)bt.B * bt.Hq : 0);
+    if (tasks == 0) return ALAYA_OK;
+    attend_kernel<T, D, G><<<(unsigned)((tasks + kWarps - 1) / kWarps), kThreads, 0, st>>>(
+        bt, q, smax, ws, want_values);
     return cuda_check("attend_kernel");
   }
-  static int combine(const Batch& bt, const float* q, const float* smax, const Ws& ws, float* out,
+  static int combine(const Batch& bt, const float* smax, const Ws& ws, float* out,
                      float* part_out, float* smax_out, cudaStream_t st) {
-    combine_kernel<T, D, G><<<bt.B * bt.Hkv, kThreads, 0, st>>>(bt, q, smax, ws, out, part_out,
-                                                                smax_out);
+    const int rows = bt.B * bt.Hq;
+    combine_kernel<D, G><<<rows, kThreads, 0, st>>>(bt, smax, ws, out, part_out, smax_out);
     return cuda_check("combine_kernel");
   }
 };
 
 using ScanFn = int (*)(const Batch&, const float*, const Ws&, cudaStream_t);
-using AttendFn = int (*)(const Batch&, const float*, const Ws&, int, cudaStream_t);
-using CombineFn = int (*)(const Batch&, const float*, const float*, const Ws&, float*, float*,
-                          float*, cudaStream_t);
+using AttendFn = int (*)(const Batch&, const float*, const float*, const Ws&, int, cudaStream_t);
+using CombineFn = int (*)(const Batch&, const float*, const Ws&, float*, float*, float*,
+                          cudaStream_t);
 
 struct StageSet {
   ScanFn scan;
@@ -80,6 +76,9 @@ StageSet pick_g(int G) {
   X(f32_16) X(f32_32) X(f32_64) X(f32_128) X(f32_256)                              \
   X(bf16_16) X(bf16_32) X(bf16_64) X(bf16_128) X(bf16_256)
 #define ALAYA_DECL(name) StageSet pick_##name(int G);
+bool tc_scan_eligible(const Batch& bt, int dtype, const alaya_seq* seqs);
+int launch_tc_scan(const Batch& bt, const alaya_seq* seqs, const float* q, const Ws& ws,
+                   cudaStream_t st);
 ALAYA_DECLARE_PICKS(ALAYA_DECL)
 #undef ALAYA_DECL
 

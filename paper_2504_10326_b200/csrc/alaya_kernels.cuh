@@ -178,231 +178,157 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
 
 // ---------------------------------------------------------------------------
 // Stage 2: exact filter + V gather (reference: dipr.py:64, store.py:271-278,
-// attention.py:98-110). Softmax reference point is the (global) max, so the
-// chunk partials need no rescaling when merged.
+// attention.py:98-110). One WARP per task; tasks [0, chunks*G) are
+// (chunk, query head) pairs, tasks [chunks*G, chunks*G + B*Hq) compute the
+// window partial of one (sequence, query head). Softmax reference point of a
+// selection partial is the (global) max, so chunk partials merge by plain sums.
 // ---------------------------------------------------------------------------
-template <typename T, int D, int G>
-__global__ void __launch_bounds__(kThreads)
-    attend_kernel(const __grid_constant__ Batch bt, const float* __restrict__ smax_ext, Ws ws,
-                  int want_values) {
-  extern __shared__ float smem[];
+constexpr int kGatherU = 16;  // V rows in flight per half-warp (one candidate batch)
+
+constexpr int kWinU = 4;     // window rows in flight per half-warp
+
+template <typename T, int D>
+__device__ __forceinline__ void hw_dot_rows(const T* const (&rows)[kWinU], const float (&qr)[D / 16],
+                                            float (&out)[kWinU], int hl) {
   constexpr int DPL = D / 16;
-  const int chunk = bt.chunk;
-  const int nwords = chunk / 32;
-  float* wt = smem;                                   // [G][chunk] weights (0 = not selected)
-  const int wt_floats = max(G * chunk, kWarps * G * D);
-  uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem + wt_floats);  // [chunk/32]
-  int* ulist = reinterpret_cast<int*>(bitmap + nwords);               // [chunk]
-  int* wsc = ulist + chunk;                                           // [kWarps]
-  int* wrc = wsc + kWarps;                                            // [kWarps]
-  float* fred = reinterpret_cast<float*>(wrc + kWarps);               // [kWarps]
-  int* nu_s = reinterpret_cast<int*>(fred + kWarps);                  // [1]
-
-  int b, h, ci;
-  decode_chunk(bt, blockIdx.x, b, h, ci);
-  const KSeq& s = bt.s[b];
-  const int t0 = ci * chunk;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const float k2 = bt.inv_sqrt_d * kLog2e;
-  const size_t cbase = (size_t)blockIdx.x * G;
-
-  if (want_values) {
-    for (int i = tid; i < G * chunk; i += kThreads) wt[i] = 0.f;
-    for (int i = tid; i < nwords; i += kThreads) bitmap[i] = 0u;
-  }
-  __syncthreads();
-
-#pragma unroll 1
-  for (int j = 0; j < G; ++j) {
-    const int qh = h * G + j;
-    const float smax = smax_ext ? smax_ext[b * bt.Hq + qh] : dec_max(ws.gmax[b * bt.Hq + qh]);
-    const float th = smax - bt.beta;
-    const int nc = ws.cnt[cbase + j];
-    int* ci_ = ws.cidx + (cbase + j) * chunk;
-    const float* cs_ = ws.cscore + (cbase + j) * chunk;
-    int sel_tot = 0, ret_tot = 0;
-    float lsum = 0.f;
-    for (int r0 = 0; r0 < nc; r0 += kThreads) {
-      const int i = r0 + tid;
-      const bool valid = i < nc;
-      const int t = valid ? ci_[i] : 0;
-      const float sv = valid ? cs_[i] : -INFINITY;
-      const bool pass = valid && sv >= th;
-      const bool sel = pass && !in_window(s.off + t0 + t, s.P, bt.wi, bt.wl);
-      const unsigned bs = __ballot_sync(kFull, sel), br = __ballot_sync(kFull, pass);
-      if (lane == 0) { wsc[warp] = __popc(bs); wrc[warp] = __popc(br); }
-      if (sel && want_values) {
-        const float w = exp2f((sv - smax) * k2);
-        wt[j * chunk + t] = w;
-        atomicOr(&bitmap[t >> 5], 1u << (t & 31));
-        lsum += w;
-      }
-      __syncthreads();
-      int off = sel_tot, add_s = 0, add_r = 0;
+  RawFrag<T, DPL> f[kWinU];
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        off += (w < warp) ? wsc[w] : 0;
-        add_s += wsc[w];
-        add_r += wrc[w];
-      }
-      if (sel) ci_[off + __popc(bs & lanemask_lt())] = t;  // in place, ascending
-      sel_tot += add_s;
-      ret_tot += add_r;
-      __syncthreads();
-    }
-    if (tid == 0) { ws.selcnt[cbase + j] = sel_tot; ws.retcnt[cbase + j] = ret_tot; }
-    if (want_values) {
-      const float l = block_sum(lsum, fred);
-      if (tid == 0) ws.part_l[cbase + j] = l;
-    }
-  }
-  if (!want_values) return;
-  __syncthreads();
-
-  // union of the group's selections, ascending local rows
-  if (warp == 0) {
-    int run = 0;
-    for (int w0 = 0; w0 < nwords; w0 += 32) {
-      const int wi = w0 + lane;
-      const uint32_t bits = wi < nwords ? bitmap[wi] : 0u;
-      int c = __popc(bits), incl = c;
-#pragma unroll
-      for (int m = 1; m < 32; m <<= 1) {
-        int o = __shfl_up_sync(kFull, incl, m);
-        if (lane >= m) incl += o;
-      }
-      int pos = run + incl - c;
-      uint32_t x = bits;
-      while (x) {
-        int bit = __ffs(x) - 1;
-        ulist[pos++] = wi * 32 + bit;
-        x &= x - 1;
-      }
-      run += __shfl_sync(kFull, incl, 31);
-    }
-    if (lane == 0) *nu_s = run;
-  }
-  __syncthreads();
-  const int nu = *nu_s;
-
-  // V gather: a half-warp per row, 4 rows in flight per half-warp
-  const int hw = tid >> 4, hl = tid & 15;
-  const T* vb = reinterpret_cast<const T*>(s.v) + (size_t)h * s.hs + (size_t)t0 * D + hl * DPL;
-  float acc[G][DPL];
-#pragma unroll
-  for (int j = 0; j < G; ++j)
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) acc[j][e] = 0.f;
-  constexpr int U = 4;
-  for (int u0 = hw; u0 < nu; u0 += kHalfWarps * U) {
-    RawFrag<T, DPL> f[U];
-    int tt[U];
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int u = u0 + k * kHalfWarps;
-      tt[k] = u < nu ? ulist[u] : -1;
-      if (tt[k] >= 0) f[k].load(vb + (size_t)tt[k] * D); else f[k].zero();
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      if (tt[k] < 0) continue;
-      float x[DPL];
-      f[k].to_float(x);
-#pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const float w = wt[j * chunk + tt[k]];
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) acc[j][e] = fmaf(w, x[e], acc[j][e]);
-      }
-    }
+  for (int k = 0; k < kWinU; ++k) {
+    if (rows[k]) f[k].load(rows[k] + hl * DPL); else f[k].zero();
   }
 #pragma unroll
-  for (int j = 0; j < G; ++j)
+  for (int k = 0; k < kWinU; ++k) {
+    float x[DPL];
+    f[k].to_float(x);
+    float a = 0.f;
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) acc[j][e] += __shfl_xor_sync(kFull, acc[j][e], 16);
-  __syncthreads();  // wt reads finished: reuse it as [kWarps][G][D]
-  float* red = wt;
-  if (lane < 16) {
+    for (int e = 0; e < DPL; ++e) a = fmaf(qr[e], x[e], a);
 #pragma unroll
-    for (int j = 0; j < G; ++j)
-#pragma unroll
-      for (int e = 0; e < DPL; ++e) red[(warp * G + j) * D + hl * DPL + e] = acc[j][e];
-  }
-  __syncthreads();
-  for (int idx = tid; idx < G * D; idx += kThreads) {
-    float t = 0.f;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) t += red[w * G * D + idx];
-    ws.part_acc[cbase * D + idx] = t;
+    for (int m = 8; m > 0; m >>= 1) a += __shfl_xor_sync(kFull, a, m);
+    out[k] = a;
   }
 }
 
-// ---------------------------------------------------------------------------
-// Stage 3: per (sequence, kv head): chunk partials + window partial, merged
-// (attention.py:128-143: selected first, then window) and finalized
-// (attention.py:145-152) or exported as (m, l, acc) for a cross-shard merge.
-// ---------------------------------------------------------------------------
-constexpr int kWinBatch = 64;
-
 template <typename T, int D, int G>
-__global__ void __launch_bounds__(kThreads)
-    combine_kernel(const __grid_constant__ Batch bt, const float* __restrict__ q,
-                   const float* __restrict__ smax_ext, Ws ws, float* __restrict__ out,
-                   float* __restrict__ part_out, float* __restrict__ smax_out) {
+__global__ void __launch_bounds__(kThreads, 2)
+    attend_kernel(const __grid_constant__ Batch bt, const float* __restrict__ q,
+                  const float* __restrict__ smax_ext, Ws ws, int want_values) {
   constexpr int DPL = D / 16;
-  __shared__ float accb[G * D];
-  __shared__ float accw[G * D];
-  __shared__ float zb[G][kWinBatch];
-  __shared__ float mw[G], lw[G], scl[G], lb[G], zmax[G];
+  __shared__ int s_t[kWarps][32];
+  __shared__ float s_w[kWarps][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int hl = lane & 15, half = lane >> 4;
+  const int task = blockIdx.x * kWarps + warp;
+  const int nsel_tasks = bt.total_chunks * G;
 
-  const int b = blockIdx.x / bt.Hkv, h = blockIdx.x - b * bt.Hkv;
-  const KSeq& s = bt.s[b];
-  const int tid = threadIdx.x, hw = tid >> 4, hl = tid & 15;
-  const int c0 = s.chunk_base + h * s.nch;
-
-  // base (selected-set) partial: sum over chunks in order, reference point = max
-  for (int idx = tid; idx < G * D; idx += kThreads) {
-    const int j = idx / D, e = idx - j * D;
-    float t = 0.f;
-    for (int c = 0; c < s.nch; ++c) t += ws.part_acc[((size_t)(c0 + c) * G + j) * D + e];
-    accb[idx] = t;
-    accw[idx] = 0.f;
-  }
-  if (tid < G) {
-    const int qh = h * G + tid;
-    float l = 0.f;
-    int sel = 0, ret = 0;
-    for (int c = 0; c < s.nch; ++c) {
-      l += ws.part_l[(size_t)(c0 + c) * G + tid];
-      sel += ws.selcnt[(size_t)(c0 + c) * G + tid];
-      ret += ws.retcnt[(size_t)(c0 + c) * G + tid];
-    }
+  if (task < nsel_tasks) {
+    // ---- selection partial of (chunk c, head j) ----
+    const int c = task / G, j = task - c * G;
+    int b, h, ci;
+    decode_chunk(bt, c, b, h, ci);
+    const KSeq& s = bt.s[b];
+    const int chunk = bt.chunk;
+    const int t0 = ci * chunk;
+    const int qh = h * G + j;
     const float smax = smax_ext ? smax_ext[b * bt.Hq + qh] : dec_max(ws.gmax[b * bt.Hq + qh]);
-    if (smax_out) smax_out[b * bt.Hq + qh] = smax;
-    lb[tid] = (sel > 0) ? l : 0.f;
-    zmax[tid] = smax * bt.inv_sqrt_d;
-    mw[tid] = -INFINITY;
-    lw[tid] = 0.f;
+    const float th = smax - bt.beta;
+    const float k2 = bt.inv_sqrt_d * kLog2e;
+    const size_t cj = (size_t)c * G + j;
+    const int nc = ws.cnt[cj];
+    int* ci_ = ws.cidx + cj * chunk;
+    const float* cs_ = ws.cscore + cj * chunk;
+    const T* vb = reinterpret_cast<const T*>(s.v) + (size_t)h * s.hs + (size_t)t0 * D + hl * DPL;
+    float acc[DPL];
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) acc[e] = 0.f;
+    int sel_tot = 0, ret_tot = 0;
+    float lsum = 0.f;
+    int t_n = lane < nc ? ci_[lane] : 0;
+    float s_n = lane < nc ? cs_[lane] : -INFINITY;
+    for (int i0 = 0; i0 < nc; i0 += 32) {
+      const int i = i0 + lane;
+      const bool valid = i < nc;
+      const int t = t_n;
+      const float sv = s_n;
+      if (i0 + 32 < nc) {  // prefetch the next candidate batch
+        const int ii = i + 32;
+        t_n = ii < nc ? ci_[ii] : 0;
+        s_n = ii < nc ? cs_[ii] : -INFINITY;
+      }
+      const bool pass = valid && sv >= th;
+      const bool sel = pass && !in_window(s.off + t0 + t, s.P, bt.wi, bt.wl);
+      const unsigned bs = __ballot_sync(kFull, sel), br = __ballot_sync(kFull, pass);
+      const int pos = __popc(bs & lanemask_lt());
+      const int ns = __popc(bs);
+      float w = 0.f;
+      if (sel) w = exp2f((sv - smax) * k2);
+      lsum += w;
+      __syncwarp();  // all lanes have read this batch before it is overwritten
+      if (sel) {
+        ci_[sel_tot + pos] = t;  // in place, ascending
+        s_t[warp][pos] = t;
+        s_w[warp][pos] = w;
+      }
+      sel_tot += ns;
+      ret_tot += __popc(br);
+      __syncwarp();
+      if (want_values && ns > 0) {
+        // half-warp `half` takes compacted rows half, half+2, ... (<= 16 rows, one round)
+        RawFrag<T, DPL> f[kGatherU];
+        float wk[kGatherU];
+#pragma unroll
+        for (int k = 0; k < kGatherU; ++k) {
+          const int r = 2 * k + half;
+          if (r < ns) {
+            f[k].load(vb + (size_t)s_t[warp][r] * D);
+            wk[k] = s_w[warp][r];
+          } else {
+            f[k].zero();
+            wk[k] = 0.f;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kGatherU; ++k) {
+          float x[DPL];
+          f[k].to_float(x);
+#pragma unroll
+          for (int e = 0; e < DPL; ++e) acc[e] = fmaf(wk[k], x[e], acc[e]);
+        }
+      }
+      __syncwarp();
+    }
+    lsum = warp_sum(lsum);
+    if (lane == 0) {
+      ws.selcnt[cj] = sel_tot;
+      ws.retcnt[cj] = ret_tot;
+      if (want_values) ws.part_l[cj] = lsum;
+    }
+    if (want_values) {
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) acc[e] += __shfl_xor_sync(kFull, acc[e], 16);
+      if (half == 0) {
+        float* pa = ws.part_acc + cj * D + hl * DPL;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) pa[e] = acc[e];
+      }
+    }
+    return;
   }
 
-  // window rows owned here: base window ids inside [off, off+n), then session rows
+  // ---- window partial of (sequence b, query head qh): base window ids owned
+  // here + session rows, online softmax in batches of 2*kWinU rows ----
+  const int wt = task - nsel_tasks;
+  if (!want_values || wt >= bt.B * bt.Hq) return;
+  const int b = wt / bt.Hq, qh = wt - b * bt.Hq, h = qh / G;
+  const KSeq& s = bt.s[b];
   const int64_t P = s.P, off = s.off;
-  int64_t a0, a1, b0, b1;  // local row ranges [a0,a1) and [b0,b1)
-  if (P <= (int64_t)bt.wi + bt.wl) {
-    a0 = 0; a1 = P; b0 = 0; b1 = 0;
-  } else {
-    a0 = 0; a1 = bt.wi; b0 = P - bt.wl; b1 = P;
-  }
+  int64_t a0 = 0, a1, b0, b1;
+  if (P <= (int64_t)bt.wi + bt.wl) { a1 = P; b0 = 0; b1 = 0; }
+  else { a1 = bt.wi; b0 = P - bt.wl; b1 = P; }
   a0 = max(a0, off) - off; a1 = min(a1, off + s.n) - off; if (a1 < a0) a1 = a0;
   b0 = max(b0, off) - off; b1 = min(b1, off + s.n) - off; if (b1 < b0) b1 = b0;
   const int na = (int)(a1 - a0), nbw = (int)(b1 - b0);
   const int R = na + nbw + s.w;
-
-  float qr[G][DPL];
-  const float* qb = q + ((size_t)b * bt.Hq + (size_t)h * G) * D + hl * DPL;
-#pragma unroll
-  for (int j = 0; j < G; ++j) load_q<DPL>(qb + (size_t)j * D, qr[j]);
-
   const T* kbase = reinterpret_cast<const T*>(s.k) + (size_t)h * s.hs;
   const T* vbase = reinterpret_cast<const T*>(s.v) + (size_t)h * s.hs;
   const T* wkb = reinterpret_cast<const T*>(s.wk) + (size_t)h * s.whs;
@@ -412,80 +338,147 @@ __global__ void __launch_bounds__(kThreads)
     if (r < na + nbw) return (val ? vbase : kbase) + (size_t)(b0 + r - na) * D;
     return (val ? wvb : wkb) + (size_t)(r - na - nbw) * D;
   };
-  __syncthreads();
-
-  for (int r0 = 0; r0 < R; r0 += kWinBatch) {
-    const int nr = min(kWinBatch, R - r0);
-    for (int rr = hw; rr < kWinBatch; rr += kHalfWarps) {  // warp-uniform trip count
-      float sj[G];
-      RawFrag<T, DPL> f;
-      if (rr < nr) f.load(row_ptr(r0 + rr, false) + hl * DPL); else f.zero();
+  float qr[DPL];
+  load_q<DPL>(q + ((size_t)b * bt.Hq + qh) * D + hl * DPL, qr);
+  float m = -INFINITY, l = 0.f, acc[DPL];
+#pragma unroll
+  for (int e = 0; e < DPL; ++e) acc[e] = 0.f;
+  for (int r0 = 0; r0 < R; r0 += 2 * kWinU) {
+    const T* kr[kWinU];
+    const T* vr[kWinU];
+#pragma unroll
+    for (int k = 0; k < kWinU; ++k) {
+      const int r = r0 + 2 * k + half;
+      kr[k] = r < R ? row_ptr(r, false) : nullptr;
+      vr[k] = r < R ? row_ptr(r, true) : nullptr;
+    }
+    float z[kWinU];
+    hw_dot_rows<T, D>(kr, qr, z, hl);
+    float bm = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < kWinU; ++k) {
+      z[k] = kr[k] ? z[k] * bt.inv_sqrt_d : -INFINITY;
+      bm = fmaxf(bm, z[k]);
+    }
+    bm = fmaxf(bm, __shfl_xor_sync(kFull, bm, 16));
+    const float mn = fmaxf(m, bm);
+    const float sc = (m == -INFINITY) ? 0.f : expf(m - mn);
+    RawFrag<T, DPL> f[kWinU];
+#pragma unroll
+    for (int k = 0; k < kWinU; ++k) {
+      if (vr[k]) f[k].load(vr[k] + hl * DPL); else f[k].zero();
+    }
+    float lb = 0.f;
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) acc[e] *= sc;
+#pragma unroll
+    for (int k = 0; k < kWinU; ++k) {
+      const float w = kr[k] ? expf(z[k] - mn) : 0.f;
+      lb += w;
       float x[DPL];
-      f.to_float(x);
+      f[k].to_float(x);
 #pragma unroll
-      for (int j = 0; j < G; ++j) {
-        float a = 0.f;
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) a = fmaf(qr[j][e], x[e], a);
-#pragma unroll
-        for (int m = 8; m > 0; m >>= 1) a += __shfl_xor_sync(kFull, a, m);
-        sj[j] = a;
-      }
-      if (hl == 0) {
-#pragma unroll
-        for (int j = 0; j < G; ++j) zb[j][rr] = rr < nr ? sj[j] * bt.inv_sqrt_d : -INFINITY;
-      }
+      for (int e = 0; e < DPL; ++e) acc[e] = fmaf(w, x[e], acc[e]);
     }
-    __syncthreads();
-    if (tid < G) {
-      float bm = -INFINITY;
-      for (int r = 0; r < nr; ++r) bm = fmaxf(bm, zb[tid][r]);
-      const float mn = fmaxf(mw[tid], bm);
-      const float sc = (mw[tid] == -INFINITY) ? 0.f : expf(mw[tid] - mn);
-      float l = lw[tid] * sc;
-      for (int r = 0; r < nr; ++r) {
-        const float w = expf(zb[tid][r] - mn);
-        zb[tid][r] = w;
-        l += w;
-      }
-      mw[tid] = mn;
-      lw[tid] = l;
-      scl[tid] = sc;
-    }
-    __syncthreads();
-    for (int idx = tid; idx < G * D; idx += kThreads) {
-      const int j = idx / D, e = idx - j * D;
-      float a = accw[idx] * scl[j];
-      for (int r = 0; r < nr; ++r) {
-        const T* vp = row_ptr(r0 + r, true) + e;
-        float v;
-        if constexpr (std::is_same_v<T, float>) v = __ldg(vp);
-        else v = __bfloat162float(*vp);
-        a = fmaf(zb[j][r], v, a);
-      }
-      accw[idx] = a;
-    }
-    __syncthreads();
+    lb += __shfl_xor_sync(kFull, lb, 16);
+    l = l * sc + lb;
+    m = mn;
   }
+#pragma unroll
+  for (int e = 0; e < DPL; ++e) acc[e] += __shfl_xor_sync(kFull, acc[e], 16);
+  float* pr = ws.partbuf + (size_t)wt * (D + 2);
+  if (lane == 0) { pr[0] = R > 0 ? m : -INFINITY; pr[1] = R > 0 ? l : 0.f; }
+  if (half == 0) {
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) pr[2 + hl * DPL + e] = R > 0 ? acc[e] : 0.f;
+  }
+}
 
-  // merge(selected, window) then finalize / export
-  for (int idx = tid; idx < G * D; idx += kThreads) {
-    const int j = idx / D, e = idx - j * D;
-    const bool hb = lb[j] > 0.f, hwn = R > 0;
-    const float m = fmaxf(hb ? zmax[j] : -INFINITY, hwn ? mw[j] : -INFINITY);
-    const float fb = hb ? expf(zmax[j] - m) : 0.f;
-    const float fw = hwn ? expf(mw[j] - m) : 0.f;
-    const float l = lb[j] * fb + lw[j] * fw;
-    const float a = accb[idx] * fb + accw[idx] * fw;
-    const size_t row = (size_t)b * bt.Hq + h * G + j;
+// ---------------------------------------------------------------------------
+// Stage 3: one CTA per (sequence, query head): sum of the chunk partials (the
+// selected set, reference point = max; warps take interleaved chunks, fixed
+// reduction order) merged with the window partial (attention.py:128-143,
+// selected first, then window), finalized (attention.py:145-152) or exported
+// as (m, l, acc) for a cross-shard merge.
+// ---------------------------------------------------------------------------
+template <int D, int G>
+__global__ void __launch_bounds__(kThreads)
+    combine_kernel(const __grid_constant__ Batch bt, const float* __restrict__ smax_ext, Ws ws,
+                   float* __restrict__ out, float* __restrict__ part_out,
+                   float* __restrict__ smax_out) {
+  constexpr int DL = (D + 31) / 32;
+  constexpr int U = 4;
+  __shared__ float red[kWarps][D];
+  __shared__ float redl[kWarps];
+  __shared__ int redn[kWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row = blockIdx.x;
+  const int b = row / bt.Hq, qh = row - b * bt.Hq;
+  const int h = qh / G, j = qh - h * G;
+  const KSeq& s = bt.s[b];
+  const int c0 = s.chunk_base + h * s.nch;
+  float ab[DL];
+#pragma unroll
+  for (int k = 0; k < DL; ++k) ab[k] = 0.f;
+  float lb = 0.f;
+  int nsel = 0;
+  for (int c = warp; c < s.nch; c += kWarps * U) {
+    float v[U][DL];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int cc = c + u * kWarps;
+#pragma unroll
+      for (int k = 0; k < DL; ++k) {
+        const int e = lane + 32 * k;
+        v[u][k] = (cc < s.nch && e < D) ? ws.part_acc[((size_t)(c0 + cc) * G + j) * D + e] : 0.f;
+      }
+      if (lane == 0 && cc < s.nch) {
+        lb += ws.part_l[(size_t)(c0 + cc) * G + j];
+        nsel += ws.selcnt[(size_t)(c0 + cc) * G + j];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < DL; ++k) ab[k] += v[u][k];
+  }
+#pragma unroll
+  for (int k = 0; k < DL; ++k)
+    if (lane + 32 * k < D) red[warp][lane + 32 * k] = ab[k];
+  if (lane == 0) { redl[warp] = lb; redn[warp] = nsel; }
+  __syncthreads();
+  if (warp != 0) return;
+  lb = 0.f;
+  nsel = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) { lb += redl[w]; nsel += redn[w]; }
+  if (nsel == 0) lb = 0.f;
+  const float smax = smax_ext ? smax_ext[row] : dec_max(ws.gmax[row]);
+  if (smax_out && lane == 0) smax_out[row] = smax;
+  const float zmax = smax * bt.inv_sqrt_d;
+  const float* wp = ws.partbuf + (size_t)row * (D + 2);
+  const float mw = wp[0], lw = wp[1];
+  const bool hb = lb > 0.f, hwn = lw > 0.f;
+  const float m = fmaxf(hb ? zmax : -INFINITY, hwn ? mw : -INFINITY);
+  const float fb = hb ? expf(zmax - m) : 0.f;
+  const float fw = hwn ? expf(mw - m) : 0.f;
+  const float l = lb * fb + lw * fw;
+  const bool empty = !(hb || hwn);
+#pragma unroll
+  for (int k = 0; k < DL; ++k) {
+    const int e = lane + 32 * k;
+    if (e >= D) continue;
+    float sb = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) sb += red[w][e];
+    const float a = sb * fb + (hwn ? wp[2 + e] * fw : 0.f);
     if (out) {
       const float o = a / l;
       if (!isfinite(o)) atomicExch(ws.status, (int)ALAYA_ERR_NONFINITE);
-      out[row * D + e] = o;
+      out[(size_t)row * D + e] = o;
     }
     if (part_out) {
-      float* pr = part_out + row * (D + 2);
-      const bool empty = !(hb || hwn);
+      float* pr = part_out + (size_t)row * (D + 2);
       if (e == 0) { pr[0] = empty ? -INFINITY : m; pr[1] = empty ? 0.f : l; }
       pr[2 + e] = empty ? 0.f : a;
     }

@@ -1,0 +1,361 @@
+// Stage 1 on the 5th-generation tensor cores (sm_100a): persistent,
+// warp-specialised DIPR scan for bf16 keys, d = 128.
+//
+//   warp 0      TMA producer: K tiles (128 keys x 128 dims bf16 = 32 KB, two
+//               64-column boxes, 128B swizzle) into a kStages-deep smem ring.
+//   warp 1      TMEM allocator + MMA issuer: per tile 8 x tcgen05.mma
+//               (M=128 keys, N=NP, K=16) with A = K tile (K-major, SW128) and
+//               B = the GQA group's queries split into three bf16 terms
+//               (q = hi + mid + lo, residual < 2^-24 |q|), fp32 accumulators in
+//               TMEM, double buffered.
+//   warps 2-5   epilogue: tcgen05.ld one key row per thread, s_j = sum of the
+//               three split columns, tile max, ordered ballot compaction of
+//               s >= bound - beta into the candidate lists (same format as the
+//               CUDA-core scan), per-chunk atomic max.
+//
+// Products of bf16 values are exact in fp32, so the score error is the fp32
+// accumulation error of the tensor core, comparable to the CUDA-core path.
+#pragma once
+
+#include <cuda.h>
+
+#include "alaya_common.cuh"
+
+namespace alaya {
+namespace tc {
+
+constexpr int kTileKeys = 128;
+constexpr int kTileBytes = kTileKeys * 128 * 2;  // 32 KB
+constexpr int kBoxBytes = kTileBytes / 2;        // 64 columns x 128 rows
+constexpr int kThreadsTc = 192;
+constexpr int kMaxMaps = 128;
+
+struct Maps {
+  CUtensorMap m[kMaxMaps];
+  int16_t map_of_seq[ALAYA_MAX_BATCH];
+  int64_t row0_of_seq[ALAYA_MAX_BATCH];  // tensor-map row of (seq, head 0, token 0)
+  int64_t rows_per_head[ALAYA_MAX_BATCH];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                            uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+// K-major, 128B-swizzled UMMA shared-memory descriptor (SBO = 1024 B between
+// 8-row groups; LBO unused for swizzled K-major; version 1; layout SW128 = 2).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// kind::f16 instruction descriptor: D fp32, A/B bf16, both K-major, M=128, N.
+template <int N>
+__device__ __forceinline__ uint32_t idesc_bf16() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+template <int NP>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[NP]);
+template <>
+__device__ __forceinline__ void tmem_ld<16>(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+template <>
+__device__ __forceinline__ void tmem_ld<32>(uint32_t taddr, float (&v)[32]) {
+  float* lo = v;
+  float* hi = v + 16;
+  tmem_ld<16>(taddr, *reinterpret_cast<float(*)[16]>(lo));
+  tmem_ld<16>(taddr + 16, *reinterpret_cast<float(*)[16]>(hi));
+}
+
+__device__ __forceinline__ uint16_t bf16_bits(float x) {
+  return __bfloat16_as_ushort(__float2bfloat16_rn(x));
+}
+
+// Write q (G heads, fp32) as the B operand: rows split*G + j, K-major SW128,
+// two 64-column boxes of NP rows each (box stride NP*128 B).
+template <int G, int NP>
+__device__ __forceinline__ void build_b(uint8_t* bbuf, const float* __restrict__ qg, int lane) {
+  for (int idx = lane; idx < G * 128; idx += 32) {
+    const int j = idx >> 7, k = idx & 127;
+    const float x = qg[j * 128 + k];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+    const float r1 = x - __bfloat162float(hi);
+    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+    const float r2 = r1 - __bfloat162float(mid);
+    const uint16_t parts[3] = {__bfloat16_as_ushort(hi), __bfloat16_as_ushort(mid), bf16_bits(r2)};
+    const int box = k >> 6, kk = k & 63, c16 = kk >> 3, w = kk & 7;
+#pragma unroll
+    for (int sp = 0; sp < 3; ++sp) {
+      const int n = sp * G + j;
+      const int off = box * (NP * 128) + (n >> 3) * 1024 + (n & 7) * 128 + ((c16 ^ (n & 7)) << 4) + w * 2;
+      *reinterpret_cast<uint16_t*>(bbuf + off) = parts[sp];
+    }
+  }
+}
+
+template <int G, int kStages>
+__global__ void __launch_bounds__(kThreadsTc, 1)
+    scan_tc_kernel(const __grid_constant__ Batch bt, const __grid_constant__ Maps maps,
+                   const float* __restrict__ q, Ws ws) {
+  constexpr int NP = (3 * G <= 16) ? 16 : 32;
+  constexpr int kBBytes = 2 * NP * 128;  // one B operand (two boxes)
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* a_ring = smem;                                     // kStages x 32 KB
+  uint8_t* b_buf = a_ring + kStages * kTileBytes;             // 2 x kBBytes
+  uint64_t* bars = reinterpret_cast<uint64_t*>(b_buf + 2 * kBBytes);
+  // full[kStages], empty[kStages], accf[2], acce[2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  float* tmax = reinterpret_cast<float*>(tmem_slot + 4);    // [2][4][G]
+  int* wcnt = reinterpret_cast<int*>(tmax + 2 * 4 * G);      // [2][4][G]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t bar0 = smem_u32(bars);
+  auto full_bar = [&](int s) { return bar0 + 8u * s; };
+  auto empty_bar = [&](int s) { return bar0 + 8u * (kStages + s); };
+  auto accf_bar = [&](int a) { return bar0 + 8u * (2 * kStages + a); };
+  auto acce_bar = [&](int a) { return bar0 + 8u * (2 * kStages + 2 + a); };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(accf_bar(a), 1); mbar_init(acce_bar(a), 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * NP));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // zero both B operands (rows >= 3G stay zero)
+  for (int i = threadIdx.x; i < 2 * kBBytes / 16; i += kThreadsTc)
+    reinterpret_cast<uint4*>(b_buf)[i] = make_uint4(0, 0, 0, 0);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int chunk = bt.chunk;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int c = blockIdx.x; c < bt.total_chunks; c += gridDim.x) {
+        int b, h, ci;
+        decode_chunk(bt, c, b, h, ci);
+        const int valid = min(chunk, bt.s[b].n - ci * chunk);
+        const int ntiles = (valid + kTileKeys - 1) / kTileKeys;
+        const CUtensorMap* map = &maps.m[maps.map_of_seq[b]];
+        const int row0 = (int)(maps.row0_of_seq[b] + h * maps.rows_per_head[b] + (int64_t)ci * chunk);
+        for (int tl = 0; tl < ntiles; ++tl) {
+          mbar_wait(empty_bar(stage), phase ^ 1);
+          mbar_expect_tx(full_bar(stage), kTileBytes);
+          const uint32_t dst = smem_u32(a_ring + stage * kTileBytes);
+          tma_load_2d(dst, map, 0, row0 + tl * kTileKeys, full_bar(stage), pol);
+          tma_load_2d(dst + kBoxBytes, map, 64, row0 + tl * kTileKeys, full_bar(stage), pol);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    const uint32_t idesc = idesc_bf16<NP>();
+    int stage = 0, acc = 0, cidx = 0;
+    uint32_t phase = 0, aphase = 0;
+    for (int c = blockIdx.x; c < bt.total_chunks; c += gridDim.x, ++cidx) {
+      int b, h, ci;
+      decode_chunk(bt, c, b, h, ci);
+      const int valid = min(chunk, bt.s[b].n - ci * chunk);
+      const int ntiles = (valid + kTileKeys - 1) / kTileKeys;
+      uint8_t* bb = b_buf + (cidx & 1) * kBBytes;
+      for (int tl = 0; tl < ntiles; ++tl) {
+        mbar_wait(acce_bar(acc), aphase ^ 1);
+        fence_after();
+        if (tl == 0) {
+          // the MMAs that last read this B buffer (chunk cidx-2) are complete:
+          // the acc_empty wait above covers the tile two tiles back.
+          build_b<G, NP>(bb, q + ((size_t)b * bt.Hq + (size_t)h * G) * 128, lane);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+        }
+        mbar_wait(full_bar(stage), phase);
+        fence_after();
+        if (lane == 0) {
+          const uint32_t a_base = smem_u32(a_ring + stage * kTileBytes);
+          const uint32_t b_base = smem_u32(bb);
+          const uint32_t d = tmem_base + acc * NP;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t a_addr = a_base + (k >> 2) * kBoxBytes + (k & 3) * 32;
+            const uint32_t b_addr = b_base + (k >> 2) * (NP * 128) + (k & 3) * 32;
+            mma_bf16(d, sw128_desc(a_addr), sw128_desc(b_addr), idesc, k > 0 ? 1u : 0u);
+          }
+          mma_commit(empty_bar(stage));
+          mma_commit(accf_bar(acc));
+        }
+        __syncwarp();
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+    }
+  } else {
+    // ===================== epilogue (warps 2..5) =====================
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0, tcount = 0;
+    uint32_t aphase = 0;
+    for (int c = blockIdx.x; c < bt.total_chunks; c += gridDim.x) {
+      int b, h, ci;
+      decode_chunk(bt, c, b, h, ci);
+      const int valid = min(chunk, bt.s[b].n - ci * chunk);
+      const int ntiles = (valid + kTileKeys - 1) / kTileKeys;
+      float run[G];
+      int cnt[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        run[j] = dec_max(ws.gmax[b * bt.Hq + h * G + j]);  // any real max is a valid bound
+        cnt[j] = 0;
+      }
+      const size_t cbase = (size_t)c * G;
+      for (int tl = 0; tl < ntiles; ++tl, ++tcount) {
+        mbar_wait(accf_bar(acc), aphase);
+        fence_after();
+        float v[NP];
+        tmem_ld<NP>(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NP, v);
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acce_bar(acc));
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+
+        const int row = tl * kTileKeys + quarter * 32 + lane;
+        const bool ok = row < valid;
+        float sc[G];
+        const int tb = tcount & 1;
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          sc[j] = ok ? v[j] + (v[G + j] + v[2 * G + j]) : -INFINITY;
+          const float m = warp_max(sc[j]);
+          if (lane == 0) tmax[(tb * 4 + quarter) * G + j] = m;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        unsigned bal[G];
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          float tm = tmax[(tb * 4 + 0) * G + j];
+#pragma unroll
+          for (int qq = 1; qq < 4; ++qq) tm = fmaxf(tm, tmax[(tb * 4 + qq) * G + j]);
+          run[j] = fmaxf(run[j], tm);
+          const bool pass = ok && sc[j] >= run[j] - bt.beta;
+          bal[j] = __ballot_sync(kFull, pass);
+          if (lane == 0) wcnt[(tb * 4 + quarter) * G + j] = __popc(bal[j]);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          int off = cnt[j], tot = 0;
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            const int w = wcnt[(tb * 4 + qq) * G + j];
+            off += qq < quarter ? w : 0;
+            tot += w;
+          }
+          if ((bal[j] >> lane) & 1u) {
+            const int o = off + __popc(bal[j] & lanemask_lt());
+            ws.cidx[(cbase + j) * chunk + o] = row;
+            ws.cscore[(cbase + j) * chunk + o] = sc[j];
+          }
+          cnt[j] += tot;
+        }
+      }
+      // publish the chunk's max and candidate counts (identical in every thread)
+      const int et = threadIdx.x - 64;
+      if (et < G) {
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          if (j == et) {
+            atomicMax(&ws.gmax[b * bt.Hq + h * G + j], enc_max(run[j]));
+            ws.cnt[cbase + j] = cnt[j];
+          }
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * NP));
+  }
+}
+
+inline size_t tc_smem_bytes(int G, int kStages) {
+  const int NP = (3 * G <= 16) ? 16 : 32;
+  return 1024 + (size_t)kStages * kTileBytes + 2 * 2 * NP * 128 + 8 * (2 * kStages + 4) + 16 +
+         2 * 4 * G * 8 + 64;
+}
+
+}  // namespace tc
+}  // namespace alaya

@@ -1,0 +1,120 @@
+// Host launcher of the tcgen05 scan: one TMA tensor map per distinct K slab
+// (passed by value in kernel-parameter space), persistent grid of one CTA
+// per SM.
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <mutex>
+
+#include "alaya_dispatch.cuh"
+#include "alaya_tc.cuh"
+
+namespace alaya {
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+template <int G, int S>
+int launch_s(const Batch& bt, const tc::Maps& maps, const float* q, const Ws& ws, cudaStream_t st) {
+  const size_t sm = tc::tc_smem_bytes(G, S);
+  cudaFuncSetAttribute(tc::scan_tc_kernel<G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const int grid = std::min(bt.total_chunks, num_sms());
+  tc::scan_tc_kernel<G, S><<<grid, tc::kThreadsTc, sm, st>>>(bt, maps, q, ws);
+  return cuda_check("scan_tc_kernel");
+}
+
+// pipeline depth: ALAYA_TC_STAGES (4..6) overrides the default of 6
+template <int G>
+int launch(const Batch& bt, const tc::Maps& maps, const float* q, const Ws& ws, cudaStream_t st) {
+  static const int stages = env_int("ALAYA_TC_STAGES", 6);
+  if (stages <= 4) return launch_s<G, 4>(bt, maps, q, ws, st);
+  if (stages == 5) return launch_s<G, 5>(bt, maps, q, ws, st);
+  return launch_s<G, 6>(bt, maps, q, ws, st);
+}
+
+}  // namespace
+
+bool tc_scan_eligible(const Batch& bt, int dtype, const alaya_seq* seqs) {
+  if (dtype != ALAYA_BF16 || bt.D != 128 || bt.G > 8 || bt.chunk % tc::kTileKeys) return false;
+  int distinct = 0;
+  for (int b = 0; b < bt.B; ++b) {
+    if (seqs[b].n == 0) continue;
+    if (seqs[b].head_stride % 128 || reinterpret_cast<uintptr_t>(seqs[b].k) % 16) return false;
+    bool seen = false;
+    for (int a = 0; a < b && !seen; ++a) seen = seqs[a].k == seqs[b].k;
+    distinct += !seen;
+  }
+  return distinct <= tc::kMaxMaps && encode_fn() != nullptr;
+}
+
+int launch_tc_scan(const Batch& bt, const alaya_seq* seqs, const float* q, const Ws& ws,
+                   cudaStream_t st) {
+  if (bt.total_chunks == 0) return ALAYA_OK;
+  static thread_local tc::Maps maps;  // ~19 KB: keep off the stack
+  auto enc = encode_fn();
+  // L2 sector promotion of the K boxes: ALAYA_TC_PROMO 0..3 = none/64B/128B/256B
+  static const CUtensorMapL2promotion promo =
+      static_cast<CUtensorMapL2promotion>(env_int("ALAYA_TC_PROMO", 3));
+  int nmaps = 0;
+  for (int b = 0; b < bt.B; ++b) {
+    maps.map_of_seq[b] = 0;
+    maps.row0_of_seq[b] = 0;
+    maps.rows_per_head[b] = seqs[b].head_stride / 128;
+    if (seqs[b].n == 0) continue;
+    int found = -1;
+    for (int a = 0; a < b && found < 0; ++a)
+      if (seqs[a].n && seqs[a].k == seqs[b].k) found = maps.map_of_seq[a];
+    if (found >= 0) { maps.map_of_seq[b] = (int16_t)found; continue; }
+    const cuuint64_t rows = (cuuint64_t)bt.Hkv * (seqs[b].head_stride / 128);
+    cuuint64_t gdim[2] = {128, rows};
+    cuuint64_t gstride[1] = {256};
+    cuuint32_t box[2] = {64, (cuuint32_t)tc::kTileKeys};
+    cuuint32_t estride[2] = {1, 1};
+    CUresult r = enc(&maps.m[nmaps], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(seqs[b].k),
+                     gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, promo,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(ALAYA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    maps.map_of_seq[b] = (int16_t)nmaps++;
+  }
+  switch (bt.G) {
+    case 1: return launch<1>(bt, maps, q, ws, st);
+    case 2: return launch<2>(bt, maps, q, ws, st);
+    case 3: return launch<3>(bt, maps, q, ws, st);
+    case 4: return launch<4>(bt, maps, q, ws, st);
+    case 5: return launch<5>(bt, maps, q, ws, st);
+    case 6: return launch<6>(bt, maps, q, ws, st);
+    case 7: return launch<7>(bt, maps, q, ws, st);
+    default: return launch<8>(bt, maps, q, ws, st);
+  }
+}
+
+}  // namespace alaya

@@ -252,3 +252,73 @@ def test_bf16_and_fp32_paths_agree_on_bf16_data(cuda_ok):
         s.update(c.q[0, 0], c.k[0, 0], c.v[0, 0], 0)
         outs.append(s.attention(c.q[0, 0], 0))
     assert rel(outs[0], outs[1].astype(np.float64)) <= 1e-5
+
+
+@pytest.mark.parametrize("scan", ["tcgen05", "cuda_core"])
+@pytest.mark.parametrize("g,n,beta", [(1, 1000, 20.0), (2, 4097, 110.0), (4, 70001, 110.0),
+                                      (5, 33333, 50.0), (8, 5000, 110.0), (4, 300, 1e9)])
+def test_bf16_scan_kernels_vs_oracle(cuda_ok, scan, g, n, beta):
+    """Both scan kernels on bf16 K/V (Llama/Qwen-like groups, ragged lengths) vs
+    the fp64 oracle on the same bf16-rounded inputs."""
+    import paper_2504_10326_b200 as P
+    hkv, d = 2, 128
+    shape = P.ModelShape(1, hkv * g, hkv, d)
+    cfg = P.EngineConfig(beta=beta, first_layers=(0,), short_context_threshold=0,
+                         kv_dtype="bfloat16", scan_kernel=scan)
+    db = P.ContextStore(shape, cfg)
+    tok, keys, vals, centers, _ = O.make_context(n, 1, hkv, d, seed=n + g)
+    keys, vals = O.bf16_round(keys), O.bf16_round(vals)
+    db.import_context(tok, keys, vals)
+    s, _ = db.create_session(tok)
+    r = np.random.default_rng(g)
+    q = (centers[r.integers(0, 16, hkv * g)] + 0.25 * r.standard_normal((hkv * g, d))).astype(np.float32)
+    kk = O.bf16_round(r.standard_normal((hkv, d)).astype(np.float32))
+    vv = O.bf16_round(r.standard_normal((hkv, d)).astype(np.float32))
+    s.update(q, kk, vv, 0)
+    out = s.attention(q, 0)
+    diag = s.last_diagnostics
+    ref, sels, cnts = O.session_attention_flat(q, keys[0], vals[0], kk[:, None], vv[:, None], beta)
+    flips = 0
+    for qh in range(hkv * g):
+        h = qh // g
+        got = diag["heads"][qh]["selected_base"]
+        assert boundary_ok(got, sels[qh], q[qh], keys[0, h], beta, EPS_SET["bfloat16"]), qh
+        flips += len(set(got) ^ set(sels[qh].tolist()))
+        o_ref, _, _ = O.head_attention_flat(q[qh], keys[0, h], vals[0, h], kk[h][None], vv[h][None],
+                                            beta, selected_override=got)
+        assert rel(out[qh], o_ref) <= 1e-5, (qh, rel(out[qh], o_ref))
+    assert flips <= max(2, hkv * g // 4)
+
+
+def test_tcgen05_multi_context_batch(cuda_ok):
+    """Sessions on different contexts (one TMA map each) and prefix reuse (head
+    stride > prefix) in one tcgen05 launch."""
+    import paper_2504_10326_b200 as P
+    shape = P.ModelShape(1, 8, 2, 128)
+    cfg = P.EngineConfig(beta=110.0, first_layers=(0,), short_context_threshold=0,
+                         kv_dtype="bfloat16", scan_kernel="tcgen05")
+    db = P.ContextStore(shape, cfg)
+    sessions, data = [], []
+    for i, n in enumerate([2000, 9999, 4096]):
+        tok, keys, vals, centers, _ = O.make_context(n, 1, 2, 128, seed=40 + i)
+        keys, vals = O.bf16_round(keys), O.bf16_round(vals)
+        db.import_context(tok, keys, vals)
+        reuse = tok if i != 1 else tok[:7777]  # partial prefix reuse on context 1
+        s, _ = db.create_session(reuse)
+        p = s.reused_prefix_len
+        s.plan_override = P.Plan(P.QueryKind.DIPR, P.IndexKind.FLAT, beta=110.0)
+        sessions.append(s)
+        data.append((keys[0, :, :p], vals[0, :, :p], centers))
+    r = np.random.default_rng(3)
+    q = np.stack([(c[r.integers(0, 16, 8)] + 0.25 * r.standard_normal((8, 128))) for _, _, c in data]
+                 ).astype(np.float32)
+    out = P.Session.attention_batch(sessions, q, 0)
+    for b, (keys, vals, _) in enumerate(data):
+        ref, sels, _ = O.session_attention_flat(q[b], keys, vals, None, None, 110.0)
+        diag = sessions[b].last_diagnostics
+        for qh in range(8):
+            got = diag["heads"][qh]["selected_base"]
+            assert boundary_ok(got, sels[qh], q[b, qh], keys[qh // 4], 110.0, 1e-3)
+            o_ref, _, _ = O.head_attention_flat(q[b, qh], keys[qh // 4], vals[qh // 4], None, None,
+                                                110.0, selected_override=got)
+            assert rel(out[b, qh], o_ref) <= 1e-5
