@@ -292,8 +292,8 @@ def main():
                                w=a.window_rows if kv_ring_owner else 0) for b in range(B)]
         calls.append(engine.Call(seqs, params, dtype, dev))
     out = torch.empty(L, B, Hq, d, dtype=torch.float32, device=dev)
-    smax_buf = torch.empty(L, B, Hq, dtype=torch.float32, device=dev)
-    parts = torch.empty(world, B * Hq, d + 2, dtype=torch.float32, device=dev)
+    from paper_2504_10326_b200.sharded import EngineStages, sharded_attention
+    stages = [EngineStages.from_call(c) for c in calls]
 
     def step(s):
         w = a.window_rows + s + 1
@@ -304,12 +304,8 @@ def main():
                 calls[l].set_window_rows(w)
             if world == 1:
                 calls[l].dipr_attention(Q[s, l], out=out[l])
-            else:
-                sm = calls[l].scan(Q[s, l])
-                dist.all_reduce(sm, op=dist.ReduceOp.MAX)
-                part = calls[l].attend(Q[s, l], sm)
-                dist.all_gather_into_tensor(parts, part)
-                out[l].view(B * Hq, d).copy_(engine.merge_partials(parts, d))
+            else:  # scan -> NCCL max-allreduce -> attend -> allgather -> merge
+                out[l].copy_(sharded_attention(stages[l], Q[s, l]))
 
     for s in range(a.warmup):
         step(s)

@@ -1,0 +1,100 @@
+"""Sequence-sharded decode over several GPUs of one box (north star item 4).
+
+Rank ``r`` of ``R`` holds tokens ``[lo_r, hi_r)`` of every sequence's base
+prefix (``shard_bounds``); global ids are ``token_offset + local row``, the
+same idea as ``dipr_bruteforce(token_ids=...)`` in the reference
+(``dipr.py:51,67-70``). Per layer:
+
+1. local scan -> per (sequence, q head) local max (``alaya_scan``);
+2. ``all_reduce(MAX)`` of ``[B, Hq]`` fp32 -> exactly the reference's global
+   ``scores.max()`` over the whole prefix (``dipr.py:64``);
+3. local exact filter at the global ``max - beta``, V gather and the window
+   rows this shard owns (base ids ``[0, initial)`` live on the shard holding
+   them, ``[p - last, p)`` likewise, session rows on the last rank) ->
+   one (m, l, acc) partial per q head (``alaya_attend``);
+4. ``all_gather`` of the partials and an in-order ``PartialAttention.merge``
+   + ``finalize`` (``attention.py:128-152``; merge is associative and
+   commutative, reference ``tests/test_attention.py:162-182``).
+
+Both collectives are latency-bound (128 B and ~16.6 KB per rank at B=1,
+Llama shape). The orchestration is generic over the local stages so that
+CPU (gloo) tests can drive it with a host double; the product path passes
+:class:`EngineStages`, i.e. the CUDA kernels.
+"""
+
+from __future__ import annotations
+
+from typing import Protocol
+
+import torch
+import torch.distributed as dist
+
+from . import engine
+
+
+def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous split of ``n`` tokens; the first ``n % world`` shards get one more."""
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world {world}")
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+class LocalStages(Protocol):
+    def scan(self, q: torch.Tensor) -> torch.Tensor: ...            # [B, Hq] local max
+    def attend(self, q: torch.Tensor, smax: torch.Tensor) -> torch.Tensor: ...  # [B*Hq, d+2]
+    def merge(self, parts: torch.Tensor) -> torch.Tensor: ...       # [R, B*Hq, d+2] -> [B*Hq, d]
+
+
+class EngineStages:
+    """The CUDA kernels behind :class:`LocalStages` for one layer's local shards."""
+
+    def __init__(self, seqs: list[engine.SeqView], params, dtype: torch.dtype,
+                 device: torch.device):
+        self.call = engine.Call(seqs, params, dtype, device)
+        self.dim = params.dim
+
+    @classmethod
+    def from_call(cls, call: engine.Call) -> "EngineStages":
+        self = cls.__new__(cls)
+        self.call, self.dim = call, call.params.dim
+        return self
+
+    def scan(self, q):
+        return self.call.scan(q)
+
+    def attend(self, q, smax):
+        return self.call.attend(q, smax, want_values=True)
+
+    def merge(self, parts):
+        return engine.merge_partials(parts, self.dim)
+
+
+def sharded_attention(stages: LocalStages, q: torch.Tensor, group=None) -> torch.Tensor:
+    """One decode step of one layer over sequence-sharded KV -> ``[B, Hq, d]``
+    (identical on every rank)."""
+    world = dist.get_world_size(group)
+    smax = stages.scan(q)
+    dist.all_reduce(smax, op=dist.ReduceOp.MAX, group=group)
+    part = stages.attend(q, smax)
+    part = part.contiguous()
+    parts = torch.empty((world * part.shape[0],) + tuple(part.shape[1:]), dtype=part.dtype,
+                        device=part.device)
+    dist.all_gather_into_tensor(parts, part, group=group)
+    out = stages.merge(parts.view((world,) + tuple(part.shape)))
+    return out.view(q.shape[0], q.shape[1], -1)
+
+
+def local_view(k_full: torch.Tensor, v_full: torch.Tensor, world: int, rank: int,
+               wk: torch.Tensor | None = None, wv: torch.Tensor | None = None,
+               w: int = 0) -> engine.SeqView:
+    """This rank's shard of one sequence at one layer. ``k_full`` is
+    ``[Hkv, n, d]``; the session window (``wk``/``wv``, ``w`` rows) is owned by
+    the last rank."""
+    n = k_full.shape[1]
+    lo, hi = shard_bounds(n, world, rank)
+    last = rank == world - 1
+    return engine.SeqView(k=k_full[:, lo:hi], v=v_full[:, lo:hi], n=hi - lo,
+                          wk=wk if last else None, wv=wv if last else None,
+                          w=w if last else 0, token_offset=lo, prefix_len=n)

@@ -1,0 +1,77 @@
+"""Sequence-sharded mode on ONE GPU: R shards run sequentially through the CUDA
+stages (alaya_scan / alaya_attend with token offsets), host-side max over the
+shards stands in for the NCCL max-allreduce, the stacked partials for the
+allgather; the merge runs in alaya_merge_partials. Must equal the unsharded
+kernel path and the CPU oracle (SURVEY.md §4 "single-GPU shard emulation")."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import alaya_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.mark.parametrize("kv", ["bfloat16", "float32"])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_shard_emulation_matches_unsharded(cuda_ok, kv, world):
+    from paper_2504_10326_b200 import engine
+    from paper_2504_10326_b200.sharded import EngineStages, local_view, shard_bounds
+    dev = torch.device("cuda")
+    dtype = torch.bfloat16 if kv == "bfloat16" else torch.float32
+    B, hkv, g, d, n, w, beta = 2, 2, 4, 128, 20000, 3, 110.0
+    r = np.random.default_rng(world)
+    keys, vals, qs, wks, wvs = [], [], [], [], []
+    for b in range(B):
+        _, k, v, centers, _ = O.make_context(n, 1, hkv, d, seed=100 + b)
+        if kv == "bfloat16":
+            k, v = O.bf16_round(k), O.bf16_round(v)
+        keys.append(k[0]); vals.append(v[0])
+        qs.append(centers[r.integers(0, 16, hkv * g)] + 0.25 * r.standard_normal((hkv * g, d)))
+        wks.append(O.bf16_round(r.standard_normal((hkv, w, d)).astype(np.float32)))
+        wvs.append(O.bf16_round(r.standard_normal((hkv, w, d)).astype(np.float32)))
+    q = torch.tensor(np.stack(qs), dtype=torch.float32, device=dev)
+    K = [torch.from_numpy(k).to(dev, dtype) for k in keys]
+    V = [torch.from_numpy(v).to(dev, dtype) for v in vals]
+    WK = [torch.from_numpy(x).to(dev, dtype) for x in wks]
+    WV = [torch.from_numpy(x).to(dev, dtype) for x in wvs]
+    params = engine.make_params(hkv * g, hkv, d, dtype, beta, 16, 64)
+
+    # unsharded reference run through the same kernels
+    full = engine.Call([engine.SeqView(k=K[b], v=V[b], n=n, wk=WK[b], wv=WV[b], w=w)
+                        for b in range(B)], params, dtype, dev)
+    o_full = full.dipr_attention(q).cpu().numpy()
+
+    stages = [EngineStages([local_view(K[b], V[b], world, rk, WK[b], WV[b], w) for b in range(B)],
+                           params, dtype, dev) for rk in range(world)]
+    # each shard needs its own workspace: the stages run interleaved
+    for st in stages:
+        st.call.ws = torch.empty(st.call.ws_bytes, dtype=torch.uint8, device=dev)
+    smax = torch.stack([st.scan(q) for st in stages]).amax(0)           # all_reduce(MAX)
+    parts = torch.stack([st.attend(q, smax) for st in stages])          # all_gather
+    o_sh = stages[0].merge(parts).view(B, hkv * g, d).cpu().numpy()
+
+    sel_sh = [[[] for _ in range(hkv * g)] for _ in range(B)]
+    for rk, st in enumerate(stages):
+        lo, hi = shard_bounds(n, world, rk)
+        ids, nsel, _ = st.call.selected(hi - lo)
+        ids, nsel = ids.cpu().numpy(), nsel.cpu().numpy()
+        for b in range(B):
+            for qh in range(hkv * g):
+                row = b * hkv * g + qh
+                sel_sh[b][qh].extend(ids[row, : nsel[row]].tolist())
+    for b in range(B):
+        ref, sels, _ = O.session_attention_flat(qs[b].astype(np.float32), keys[b], vals[b],
+                                                wks[b], wvs[b], beta)
+        for qh in range(hkv * g):
+            assert sorted(sel_sh[b][qh]) == sel_sh[b][qh]  # ascending across shards
+            assert len(set(sel_sh[b][qh]) ^ set(sels[qh].tolist())) <= 1
+            assert rel(o_sh[b, qh], ref[qh]) <= 1e-5 + (1e-5 if kv == "bfloat16" else 0)
+            assert rel(o_sh[b, qh], o_full[b, qh]) <= 2e-6
