@@ -132,7 +132,8 @@ int alaya_merge_states(const float* d_parts, int n_parts, int rows, int dim, flo
                        void* stream);
 
 /* After alaya_attend on the same workspace: per (seq, q head) selected ids
- * (global, ascending) into d_ids[(b*Hq+qh)*cap ...], counts into
+ * (global; deterministic order, ascending within each scan sub-list -- sort
+ * for the reference's sorted lists) into d_ids[(b*Hq+qh)*cap ...], counts into
  * d_selected[b*Hq+qh] and the retrieved count (including window ids) into
  * d_retrieved[b*Hq+qh]. cap must be >= max prefix rows per shard. */
 int alaya_selected(const alaya_params* p, const alaya_seq* seqs, int batch, int64_t* d_ids,

@@ -80,8 +80,11 @@ int build_batch(const alaya_params* p, const alaya_seq* seqs, int B, Batch* bt) 
   if (chunk > 0) {
     if (chunk % 256 || chunk > 8192) return fail(ALAYA_ERR_ARG, "chunk must be a multiple of 256, <= 8192");
   } else {
+    // the tcgen05 scan splits a chunk into 4 lane-quarter sub-lists of 128-key tiles
+    const int min_chunk =
+        (p->dtype == ALAYA_BF16 && p->dim == 128 && p->scan_kind != ALAYA_SCAN_CUDA_CORE) ? 512 : 256;
     chunk = 2048;
-    while (chunk > 256 && chunks_for(seqs, B, p->n_kv_heads, chunk) < 4 * kNumSMs) chunk >>= 1;
+    while (chunk > min_chunk && chunks_for(seqs, B, p->n_kv_heads, chunk) < 4 * kNumSMs) chunk >>= 1;
   }
   if (G * chunk * 4 > 160 * 1024) chunk = ((160 * 1024 / 4 / G) / 256) * 256;
   (void)tokens;
@@ -117,7 +120,8 @@ int build_batch(const alaya_params* p, const alaya_seq* seqs, int B, Batch* bt) 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t status, gmax, cnt, selcnt, retcnt, part_l, part_acc, cidx, cscore, partbuf, smaxbuf,
+  size_t zero_bytes;
+  size_t status, gmax, counters, cnt, selcnt, retcnt, part_l, part_acc, cidx, cscore, partbuf, smaxbuf,
       bfkeep, total;
 };
 
@@ -126,8 +130,10 @@ Layout layout_for(const Batch& bt) {
   const size_t C = (size_t)bt.total_chunks, G = bt.G, D = bt.D, rows = (size_t)bt.B * bt.Hq;
   size_t o = 0;
   L.status = o; o = align_up(o + 4);
-  L.gmax = o; o = align_up(o + 4 * rows);
-  L.cnt = o; o = align_up(o + 4 * C * G);
+  L.gmax = o; L.counters = o + 4 * rows;
+  L.zero_bytes = 4 * rows + 64 + 4 * (size_t)bt.B * bt.Hkv;  // gmax + counters + group_done
+  o = align_up(o + L.zero_bytes);
+  L.cnt = o; o = align_up(o + 4 * C * G * 4);
   L.selcnt = o; o = align_up(o + 4 * C * G);
   L.retcnt = o; o = align_up(o + 4 * C * G);
   L.part_l = o; o = align_up(o + 4 * C * G);
@@ -146,6 +152,8 @@ Ws carve(const Layout& L, void* base) {
   Ws w;
   w.status = reinterpret_cast<int*>(c + L.status);
   w.gmax = reinterpret_cast<uint32_t*>(c + L.gmax);
+  w.counters = reinterpret_cast<int*>(c + L.counters);
+  w.group_done = w.counters + 16;
   w.cnt = reinterpret_cast<int*>(c + L.cnt);
   w.selcnt = reinterpret_cast<int*>(c + L.selcnt);
   w.retcnt = reinterpret_cast<int*>(c + L.retcnt);
@@ -202,7 +210,8 @@ int prepare(const alaya_params* p, const alaya_seq* seqs, int B, void* d_ws, siz
 
 int run_scan(Call& c, const float* d_q) {
   const size_t rows = (size_t)c.bt.B * c.bt.Hq;
-  if (cudaMemsetAsync(c.ws.gmax, 0, 4 * rows, c.stream) != cudaSuccess) return cuda_check("memset");
+  (void)rows;
+  if (cudaMemsetAsync(c.ws.gmax, 0, c.L.zero_bytes, c.stream) != cudaSuccess) return cuda_check("memset");
   if (c.use_tc) return launch_tc_scan(c.bt, c.seqs, d_q, c.ws, c.stream);
   return c.st.scan(c.bt, d_q, c.ws, c.stream);
 }
@@ -233,6 +242,11 @@ int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch
   for (int b = 0; b < batch; ++b)
     if (seqs[b].prefix_len + seqs[b].w == 0) return fail(ALAYA_ERR_ARG, "attention on an empty session");
   if (cudaMemsetAsync(c.ws.status, 0, 4, c.stream) != cudaSuccess) return cuda_check("memset");
+  if (c.use_tc && fused_enabled()) {  // scan + attend in one persistent kernel
+    if (cudaMemsetAsync(c.ws.gmax, 0, c.L.zero_bytes, c.stream) != cudaSuccess) return cuda_check("memset");
+    if ((rc = launch_tc_fused(c.bt, c.seqs, d_q, c.ws, c.stream))) return rc;
+    return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);
+  }
   if ((rc = run_scan(c, d_q))) return rc;
   if ((rc = c.st.attend(c.bt, d_q, nullptr, c.ws, 1, c.stream))) return rc;
   return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);

@@ -40,13 +40,16 @@ struct Batch {
   int32_t wi, wl;
   int32_t total_chunks;
   float inv_sqrt_d;
+  int32_t dbg;  // diagnostics only (ALAYA_TC_DBG): bit0 no L2 hint, bit1 no epilogue math, bit2 no MMA
 };
 
 // Workspace pointers (device), carved from the caller's buffer.
 struct Ws {
   int* status;
   uint32_t* gmax;   // [B*Hq] order-preserving encoded running max
-  int* cnt;         // [chunks*G] candidate counts
+  int* counters;    // [16] right after gmax (zeroed with it): [0] attend ticket, [1] scan ticket
+  int* group_done;  // [B*Hkv] right after counters (zeroed with it): chunks published per group
+  int* cnt;         // [chunks*G*4] candidate counts per scan sub-list (see CandList)
   int* selcnt;      // [chunks*G]
   int* retcnt;      // [chunks*G]
   float* part_l;    // [chunks*G]
@@ -85,6 +88,70 @@ __device__ __forceinline__ void decode_chunk(const Batch& bt, int c, int& b, int
 __device__ __forceinline__ bool in_window(int64_t gid, int64_t P, int wi, int wl) {
   if (P <= (int64_t)wi + wl) return true;
   return gid < wi || gid >= P - wl;
+}
+
+// Candidate lists of one (chunk, head) pair cj: up to 4 ordered sub-lists (one
+// per tcgen05 scan epilogue warp; the CUDA-core scan writes only sub-list 0),
+// sub-list q at cidx + cj*chunk + q*(chunk/4) with count cnt[cj*4 + q]. The
+// attend stage walks them as one virtual list; its physical position of a
+// virtual index is >= the index, so selected ids can be compacted in place.
+struct CandList {
+  int pre[5];
+  int qcap;
+  __device__ __forceinline__ int total() const { return pre[4]; }
+  __device__ __forceinline__ int phys(int i) const {  // static indexing: stays in registers
+    if (i < pre[1]) return i;
+    if (i < pre[2]) return qcap + i - pre[1];
+    if (i < pre[3]) return 2 * qcap + i - pre[2];
+    return 3 * qcap + i - pre[3];
+  }
+};
+__device__ __forceinline__ CandList cand_list(const int* cnt4, int chunk, bool through_l2) {
+  CandList L;
+  L.qcap = chunk / 4;
+  L.pre[0] = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) L.pre[q + 1] = L.pre[q] + (through_l2 ? __ldcg(cnt4 + q) : cnt4[q]);
+  return L;
+}
+
+// --- mbarriers and bulk async copies (TMA engine) ---------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// 1-D bulk copy global -> shared, completing on an mbarrier (SASS UBLKCP).
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // --- streaming loads -------------------------------------------------------

@@ -10,6 +10,7 @@
 namespace alaya {
 
 int fail(int code, const char* fmt, ...);
+int num_sms();
 int cuda_check(const char* what);
 
 inline size_t scan_smem(const Batch& bt) {
@@ -29,8 +30,14 @@ struct Stages {
                     int want_values, cudaStream_t st) {
     const long tasks = (long)bt.total_chunks * G + (want_values ? (long)bt.B * bt.Hq : 0);
     if (tasks == 0) return ALAYA_OK;
-    attend_kernel<T, D, G><<<(unsigned)((tasks + kWarps - 1) / kWarps), kThreads, 0, st>>>(
-        bt, q, smax, ws, want_values);
+    static int per_sm = 0;
+    if (per_sm == 0) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attend_kernel<T, D, G>, kThreads, 0);
+      if (per_sm < 1) per_sm = 1;
+    }
+    const long blocks = std::min<long>((tasks + kWarps - 1) / kWarps, (long)per_sm * num_sms());
+    if (cudaMemsetAsync(ws.counters, 0, sizeof(int), st) != cudaSuccess) return cuda_check("memset");
+    attend_kernel<T, D, G><<<(unsigned)blocks, kThreads, 0, st>>>(bt, q, smax, ws, want_values);
     return cuda_check("attend_kernel");
   }
   static int combine(const Batch& bt, const float* smax, const Ws& ws, float* out,
@@ -79,6 +86,9 @@ StageSet pick_g(int G) {
 bool tc_scan_eligible(const Batch& bt, int dtype, const alaya_seq* seqs);
 int launch_tc_scan(const Batch& bt, const alaya_seq* seqs, const float* q, const Ws& ws,
                    cudaStream_t st);
+int launch_tc_fused(const Batch& bt, const alaya_seq* seqs, const float* q, const Ws& ws,
+                    cudaStream_t st);
+bool fused_enabled();
 ALAYA_DECLARE_PICKS(ALAYA_DECL)
 #undef ALAYA_DECL
 

@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
         off += __popc(bal);
       }
     }
-    if (tid == 0) ws.cnt[cbase + j] = tot;
+    if (tid < 4) ws.cnt[(cbase + j) * 4 + tid] = tid == 0 ? tot : 0;
   }
 }
 
@@ -209,116 +209,135 @@ __device__ __forceinline__ void hw_dot_rows(const T* const (&rows)[kWinU], const
   }
 }
 
-template <typename T, int D, int G>
-__global__ void __launch_bounds__(kThreads, 2)
-    attend_kernel(const __grid_constant__ Batch bt, const float* __restrict__ q,
-                  const float* __restrict__ smax_ext, Ws ws, int want_values) {
-  constexpr int DPL = D / 16;
-  __shared__ int s_t[kWarps][32];
-  __shared__ float s_w[kWarps][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// Selection partial of one (chunk c, head j) task, software-pipelined so the
+// V loads of candidate batch k stay in flight while batch k+1 is filtered:
+//   issue loads(k) -> filter(k+1) -> FMA(k).
+// Rows are held in registers (kGatherU per half-warp: one 32-candidate batch).
+// L2 = true reads inputs produced by other SMs in the same launch (__ldcg).
+template <typename T, int D, int G, bool L2>
+__device__ __forceinline__ void sel_task_pipe(const Batch& bt, const float* __restrict__ smax_ext,
+                                              const Ws& ws, int st, int lane, int (*s_t)[32],
+                                              float (*s_w)[32], bool want_values) {
+  constexpr int DPL = D / 16, U = kGatherU;
   const int hl = lane & 15, half = lane >> 4;
-  const int task = blockIdx.x * kWarps + warp;
-  const int nsel_tasks = bt.total_chunks * G;
-
-  if (task < nsel_tasks) {
-    // ---- selection partial of (chunk c, head j) ----
-    const int c = task / G, j = task - c * G;
-    int b, h, ci;
-    decode_chunk(bt, c, b, h, ci);
-    const KSeq& s = bt.s[b];
-    const int chunk = bt.chunk;
-    const int t0 = ci * chunk;
-    const int qh = h * G + j;
-    const float smax = smax_ext ? smax_ext[b * bt.Hq + qh] : dec_max(ws.gmax[b * bt.Hq + qh]);
-    const float th = smax - bt.beta;
-    const float k2 = bt.inv_sqrt_d * kLog2e;
-    const size_t cj = (size_t)c * G + j;
-    const int nc = ws.cnt[cj];
-    int* ci_ = ws.cidx + cj * chunk;
-    const float* cs_ = ws.cscore + cj * chunk;
-    const T* vb = reinterpret_cast<const T*>(s.v) + (size_t)h * s.hs + (size_t)t0 * D + hl * DPL;
-    float acc[DPL];
+  const int c = st / G, j = st - c * G;
+  int b, h, ci;
+  decode_chunk(bt, c, b, h, ci);
+  const KSeq& s = bt.s[b];
+  const int chunk = bt.chunk;
+  const int t0 = ci * chunk;
+  const int qh = h * G + j;
+  const float smax = smax_ext ? smax_ext[b * bt.Hq + qh]
+                              : dec_max(L2 ? __ldcg(&ws.gmax[b * bt.Hq + qh]) : ws.gmax[b * bt.Hq + qh]);
+  const float th = smax - bt.beta;
+  const float k2 = bt.inv_sqrt_d * kLog2e;
+  const size_t cj = (size_t)c * G + j;
+  const CandList L = cand_list(ws.cnt + cj * 4, chunk, L2);
+  const int nc = L.total();
+  int* ci_ = ws.cidx + cj * chunk;
+  const float* cs_ = ws.cscore + cj * chunk;
+  auto ldi = [&](int i) { return L2 ? __ldcg(ci_ + L.phys(i)) : ci_[L.phys(i)]; };
+  auto lds = [&](int i) { return L2 ? __ldcg(cs_ + L.phys(i)) : cs_[L.phys(i)]; };
+  const T* vb = reinterpret_cast<const T*>(s.v) + (size_t)h * s.hs + (size_t)t0 * D + hl * DPL;
+  float acc[DPL];
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) acc[e] = 0.f;
-    int sel_tot = 0, ret_tot = 0;
-    float lsum = 0.f;
-    int t_n = lane < nc ? ci_[lane] : 0;
-    float s_n = lane < nc ? cs_[lane] : -INFINITY;
-    for (int i0 = 0; i0 < nc; i0 += 32) {
-      const int i = i0 + lane;
-      const bool valid = i < nc;
-      const int t = t_n;
-      const float sv = s_n;
-      if (i0 + 32 < nc) {  // prefetch the next candidate batch
-        const int ii = i + 32;
-        t_n = ii < nc ? ci_[ii] : 0;
-        s_n = ii < nc ? cs_[ii] : -INFINITY;
-      }
-      const bool pass = valid && sv >= th;
-      const bool sel = pass && !in_window(s.off + t0 + t, s.P, bt.wi, bt.wl);
-      const unsigned bs = __ballot_sync(kFull, sel), br = __ballot_sync(kFull, pass);
-      const int pos = __popc(bs & lanemask_lt());
-      const int ns = __popc(bs);
-      float w = 0.f;
-      if (sel) w = exp2f((sv - smax) * k2);
-      lsum += w;
-      __syncwarp();  // all lanes have read this batch before it is overwritten
-      if (sel) {
-        ci_[sel_tot + pos] = t;  // in place, ascending
-        s_t[warp][pos] = t;
-        s_w[warp][pos] = w;
-      }
-      sel_tot += ns;
-      ret_tot += __popc(br);
-      __syncwarp();
-      if (want_values && ns > 0) {
-        // half-warp `half` takes compacted rows half, half+2, ... (<= 16 rows, one round)
-        RawFrag<T, DPL> f[kGatherU];
-        float wk[kGatherU];
-#pragma unroll
-        for (int k = 0; k < kGatherU; ++k) {
-          const int r = 2 * k + half;
-          if (r < ns) {
-            f[k].load(vb + (size_t)s_t[warp][r] * D);
-            wk[k] = s_w[warp][r];
-          } else {
-            f[k].zero();
-            wk[k] = 0.f;
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < kGatherU; ++k) {
-          float x[DPL];
-          f[k].to_float(x);
-#pragma unroll
-          for (int e = 0; e < DPL; ++e) acc[e] = fmaf(wk[k], x[e], acc[e]);
-        }
-      }
-      __syncwarp();
+  for (int e = 0; e < DPL; ++e) acc[e] = 0.f;
+  int sel_tot = 0, ret_tot = 0;
+  float lsum = 0.f;
+  int t_n = lane < nc ? ldi(lane) : 0;
+  float s_n = lane < nc ? lds(lane) : -INFINITY;
+  int next_i0 = 0;  // first candidate index of the next batch to filter
+  // filter one batch into slot `sl`, returns its selected count
+  auto filter = [&](int sl) -> int {
+    const int i0 = next_i0;
+    next_i0 += 32;
+    const int i = i0 + lane;
+    const bool valid = i < nc;
+    const int t = t_n;
+    const float sv = s_n;
+    if (i0 + 32 < nc) {  // prefetch the batch after
+      const int ii = i + 32;
+      t_n = ii < nc ? ldi(ii) : 0;
+      s_n = ii < nc ? lds(ii) : -INFINITY;
     }
-    lsum = warp_sum(lsum);
-    if (lane == 0) {
-      ws.selcnt[cj] = sel_tot;
-      ws.retcnt[cj] = ret_tot;
-      if (want_values) ws.part_l[cj] = lsum;
+    const bool pass = valid && sv >= th;
+    const bool sel = pass && !in_window(s.off + t0 + t, s.P, bt.wi, bt.wl);
+    const unsigned bs = __ballot_sync(kFull, sel), br = __ballot_sync(kFull, pass);
+    const int pos = __popc(bs & lanemask_lt());
+    const int ns = __popc(bs);
+    const float w = sel ? exp2f((sv - smax) * k2) : 0.f;
+    lsum += w;
+    __syncwarp();  // all lanes read this batch before the in-place write
+    if (sel) {
+      ci_[sel_tot + pos] = t;  // in place; physical read position >= write position
+      s_t[sl][pos] = t;
+      s_w[sl][pos] = w;
     }
-    if (want_values) {
+    sel_tot += ns;
+    ret_tot += __popc(br);
+    __syncwarp();
+    return ns;
+  };
+  int cur = 0;
+  int ns_cur = nc > 0 ? filter(0) : 0;
+  while (true) {
+    const bool more = next_i0 < nc;
+    if (!want_values) {
+      if (!more) break;
+      ns_cur = filter(cur ^ 1);
+      cur ^= 1;
+      continue;
+    }
+    RawFrag<T, DPL> f[U];
+    float wk[U];
 #pragma unroll
-      for (int e = 0; e < DPL; ++e) acc[e] += __shfl_xor_sync(kFull, acc[e], 16);
-      if (half == 0) {
-        float* pa = ws.part_acc + cj * D + hl * DPL;
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) pa[e] = acc[e];
+    for (int k = 0; k < U; ++k) {
+      const int r = 2 * k + half;
+      if (r < ns_cur) {
+        f[k].load(vb + (size_t)s_t[cur][r] * D);
+        wk[k] = s_w[cur][r];
+      } else {
+        f[k].zero();
+        wk[k] = 0.f;
       }
     }
-    return;
+    const int ns_nxt = more ? filter(cur ^ 1) : 0;  // overlaps the loads above
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      float x[DPL];
+      f[k].to_float(x);
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) acc[e] = fmaf(wk[k], x[e], acc[e]);
+    }
+    if (!more) break;
+    cur ^= 1;
+    ns_cur = ns_nxt;
   }
+  lsum = warp_sum(lsum);
+  if (lane == 0) {
+    ws.selcnt[cj] = sel_tot;
+    ws.retcnt[cj] = ret_tot;
+    if (want_values) ws.part_l[cj] = lsum;
+  }
+  if (want_values) {
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) acc[e] += __shfl_xor_sync(kFull, acc[e], 16);
+    if (half == 0) {
+      float* pa = ws.part_acc + cj * D + hl * DPL;
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) pa[e] = acc[e];
+    }
+  }
+}
 
-  // ---- window partial of (sequence b, query head qh): base window ids owned
-  // here + session rows, online softmax in batches of 2*kWinU rows ----
-  const int wt = task - nsel_tasks;
-  if (!want_values || wt >= bt.B * bt.Hq) return;
+// Window partial of (sequence b, query head qh): base window ids owned by this
+// shard + the session rows, online softmax in batches of 2*kWinU rows; written
+// to ws.partbuf[b*Hq+qh] as (m, l, acc).
+template <typename T, int D, int G>
+__device__ __forceinline__ void win_task(const Batch& bt, const float* __restrict__ q, const Ws& ws,
+                                         int wt, int lane) {
+  constexpr int DPL = D / 16;
+  const int hl = lane & 15, half = lane >> 4;
   const int b = wt / bt.Hq, qh = wt - b * bt.Hq, h = qh / G;
   const KSeq& s = bt.s[b];
   const int64_t P = s.P, off = s.off;
@@ -391,6 +410,29 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (half == 0) {
 #pragma unroll
     for (int e = 0; e < DPL; ++e) pr[2 + hl * DPL + e] = R > 0 ? acc[e] : 0.f;
+  }
+}
+
+template <typename T, int D, int G>
+__global__ void __launch_bounds__(kThreads, 2)
+    attend_kernel(const __grid_constant__ Batch bt, const float* __restrict__ q,
+                  const float* __restrict__ smax_ext, Ws ws, int want_values) {
+  __shared__ int s_t[kWarps][2][32];
+  __shared__ float s_w[kWarps][2][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwin = want_values ? bt.B * bt.Hq : 0;
+  const int ntasks = nwin + bt.total_chunks * G;
+  for (;;) {  // dynamic tickets: window tasks first, then (chunk, head) tasks
+    int task = 0;
+    if (lane == 0) task = atomicAdd(&ws.counters[0], 1);
+    task = __shfl_sync(kFull, task, 0);
+    if (task >= ntasks) break;
+    if (task < nwin) {
+      win_task<T, D, G>(bt, q, ws, task, lane);
+    } else {
+      sel_task_pipe<T, D, G, false>(bt, smax_ext, ws, task - nwin, lane, s_t[warp], s_w[warp],
+                                    want_values != 0);
+    }
   }
 }
 

@@ -37,33 +37,6 @@ struct Maps {
   int64_t rows_per_head[ALAYA_MAX_BATCH];
 };
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      " selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
-  }
-}
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -75,6 +48,14 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
       " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_nohint(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                                   uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
       : "memory");
 }
 __device__ __forceinline__ void fence_after() {
@@ -156,8 +137,82 @@ __device__ __forceinline__ void build_b(uint8_t* bbuf, const float* __restrict__
   }
 }
 
+constexpr int kAcc = 4;  // TMEM accumulator buffers (MMA runs up to 4 tiles ahead)
+
+// One chunk of the scan epilogue for this warp's TMEM lane quarter (32 key
+// rows of every 128-key tile). No cross-warp barriers: the warp keeps its own
+// running max (a max of real scores, hence a valid lower bound of the global
+// max) and writes its own ordered candidate sub-list (CandList, q = quarter).
+template <int G, int NP>
+__device__ __forceinline__ void epilogue_chunk(const Batch& bt, const Ws& ws, int c, int quarter,
+                                               int lane, uint32_t tmem_base, uint32_t accf0,
+                                               uint32_t acce0, int& acc, uint32_t& aphase,
+                                               int& b, int& h) {
+  int ci;
+  decode_chunk(bt, c, b, h, ci);
+  const int chunk = bt.chunk;
+  const int valid = min(chunk, bt.s[b].n - ci * chunk);
+  const int ntiles = (valid + kTileKeys - 1) / kTileKeys;
+  float run[G];
+  int cnt[G];
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    run[j] = dec_max(__ldcg(&ws.gmax[b * bt.Hq + h * G + j]));
+    cnt[j] = 0;
+  }
+  const size_t cbase = (size_t)c * G;
+  const int qoff = quarter * (chunk / 4);
+  for (int tl = 0; tl < ntiles; ++tl) {
+    mbar_wait(accf0 + 8u * acc, (aphase >> acc) & 1u);
+    fence_after();
+    float v[NP];
+    tmem_ld<NP>(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NP, v);
+    fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(acce0 + 8u * acc);
+    aphase ^= 1u << acc;
+    acc = (acc + 1) % kAcc;
+    if (bt.dbg & 2) continue;
+    const int row = tl * kTileKeys + quarter * 32 + lane;
+    const bool ok = row < valid;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const float sc = ok ? v[j] + (v[G + j] + v[2 * G + j]) : -INFINITY;
+      run[j] = fmaxf(run[j], warp_max(sc));
+      const bool pass = ok && sc >= run[j] - bt.beta;
+      const unsigned bal = __ballot_sync(kFull, pass);
+      if (pass) {
+        const int o = qoff + cnt[j] + __popc(bal & lanemask_lt());
+        ws.cidx[(cbase + j) * chunk + o] = row;
+        ws.cscore[(cbase + j) * chunk + o] = sc;
+      }
+      cnt[j] += __popc(bal);
+    }
+  }
+  if (lane < G) {
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      if (j == lane) {
+        atomicMax(&ws.gmax[b * bt.Hq + h * G + j], enc_max(run[j]));
+        ws.cnt[(cbase + j) * 4 + quarter] = cnt[j];
+      }
+    }
+  }
+}
+
+// MMA issue for one tile: 8 x (M=128, N=NP, K=16) into accumulator buffer acc.
+template <int NP>
+__device__ __forceinline__ void mma_tile(uint32_t a_base, uint32_t b_base, uint32_t d, uint32_t idesc) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t a_addr = a_base + (k >> 2) * kBoxBytes + (k & 3) * 32;
+    const uint32_t b_addr = b_base + (k >> 2) * (NP * 128) + (k & 3) * 32;
+    mma_bf16(d, sw128_desc(a_addr), sw128_desc(b_addr), idesc, k > 0 ? 1u : 0u);
+  }
+}
+
 template <int G, int kStages>
-__global__ void __launch_bounds__(kThreadsTc, 1)
+__global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 3 : (kStages <= 3 ? 2 : 1)))
     scan_tc_kernel(const __grid_constant__ Batch bt, const __grid_constant__ Maps maps,
                    const float* __restrict__ q, Ws ws) {
   constexpr int NP = (3 * G <= 16) ? 16 : 32;
@@ -167,29 +222,25 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   uint8_t* a_ring = smem;                                     // kStages x 32 KB
   uint8_t* b_buf = a_ring + kStages * kTileBytes;             // 2 x kBBytes
   uint64_t* bars = reinterpret_cast<uint64_t*>(b_buf + 2 * kBBytes);
-  // full[kStages], empty[kStages], accf[2], acce[2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
-  float* tmax = reinterpret_cast<float*>(tmem_slot + 4);    // [2][4][G]
-  int* wcnt = reinterpret_cast<int*>(tmax + 2 * 4 * G);      // [2][4][G]
+  // full[kStages], empty[kStages], accf[kAcc], acce[kAcc]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2 * kAcc);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar0 = smem_u32(bars);
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (kStages + s); };
-  auto accf_bar = [&](int a) { return bar0 + 8u * (2 * kStages + a); };
-  auto acce_bar = [&](int a) { return bar0 + 8u * (2 * kStages + 2 + a); };
+  const uint32_t accf0 = bar0 + 8u * (2 * kStages), acce0 = accf0 + 8u * kAcc;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(accf_bar(a), 1); mbar_init(acce_bar(a), 4); }
+    for (int a = 0; a < kAcc; ++a) { mbar_init(accf0 + 8u * a, 1); mbar_init(acce0 + 8u * a, 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * NP));
+                 "r"(kAcc * NP));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // zero both B operands (rows >= 3G stay zero)
   for (int i = threadIdx.x; i < 2 * kBBytes / 16; i += kThreadsTc)
     reinterpret_cast<uint4*>(b_buf)[i] = make_uint4(0, 0, 0, 0);
   fence_before();
@@ -215,8 +266,13 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           mbar_wait(empty_bar(stage), phase ^ 1);
           mbar_expect_tx(full_bar(stage), kTileBytes);
           const uint32_t dst = smem_u32(a_ring + stage * kTileBytes);
-          tma_load_2d(dst, map, 0, row0 + tl * kTileKeys, full_bar(stage), pol);
-          tma_load_2d(dst + kBoxBytes, map, 64, row0 + tl * kTileKeys, full_bar(stage), pol);
+          if (bt.dbg & 1) {
+            tma_load_2d_nohint(dst, map, 0, row0 + tl * kTileKeys, full_bar(stage));
+            tma_load_2d_nohint(dst + kBoxBytes, map, 64, row0 + tl * kTileKeys, full_bar(stage));
+          } else {
+            tma_load_2d(dst, map, 0, row0 + tl * kTileKeys, full_bar(stage), pol);
+            tma_load_2d(dst + kBoxBytes, map, 64, row0 + tl * kTileKeys, full_bar(stage), pol);
+          }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -225,7 +281,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     // ===================== MMA issuer =====================
     const uint32_t idesc = idesc_bf16<NP>();
     int stage = 0, acc = 0, cidx = 0;
-    uint32_t phase = 0, aphase = 0;
+    uint32_t phase = 0, ephase = 0;
     for (int c = blockIdx.x; c < bt.total_chunks; c += gridDim.x, ++cidx) {
       int b, h, ci;
       decode_chunk(bt, c, b, h, ci);
@@ -233,11 +289,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       const int ntiles = (valid + kTileKeys - 1) / kTileKeys;
       uint8_t* bb = b_buf + (cidx & 1) * kBBytes;
       for (int tl = 0; tl < ntiles; ++tl) {
-        mbar_wait(acce_bar(acc), aphase ^ 1);
+        mbar_wait(acce0 + 8u * acc, ((ephase >> acc) & 1u) ^ 1u);
+        ephase ^= 1u << acc;
         fence_after();
         if (tl == 0) {
-          // the MMAs that last read this B buffer (chunk cidx-2) are complete:
-          // the acc_empty wait above covers the tile two tiles back.
+          // the MMAs that last read this B buffer (previous chunk of this
+          // parity) are complete: the acc_empty wait covers kAcc tiles back.
           build_b<G, NP>(bb, q + ((size_t)b * bt.Hq + (size_t)h * G) * 128, lane);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
@@ -245,116 +302,37 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         mbar_wait(full_bar(stage), phase);
         fence_after();
         if (lane == 0) {
-          const uint32_t a_base = smem_u32(a_ring + stage * kTileBytes);
-          const uint32_t b_base = smem_u32(bb);
-          const uint32_t d = tmem_base + acc * NP;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const uint32_t a_addr = a_base + (k >> 2) * kBoxBytes + (k & 3) * 32;
-            const uint32_t b_addr = b_base + (k >> 2) * (NP * 128) + (k & 3) * 32;
-            mma_bf16(d, sw128_desc(a_addr), sw128_desc(b_addr), idesc, k > 0 ? 1u : 0u);
-          }
+          if (!(bt.dbg & 4))
+            mma_tile<NP>(smem_u32(a_ring + stage * kTileBytes), smem_u32(bb), tmem_base + acc * NP, idesc);
           mma_commit(empty_bar(stage));
-          mma_commit(accf_bar(acc));
+          mma_commit(accf0 + 8u * acc);
         }
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
-        if (++acc == 2) { acc = 0; aphase ^= 1; }
+        acc = (acc + 1) % kAcc;
       }
     }
   } else {
     // ===================== epilogue (warps 2..5) =====================
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    int acc = 0, tcount = 0;
+    int acc = 0;
     uint32_t aphase = 0;
     for (int c = blockIdx.x; c < bt.total_chunks; c += gridDim.x) {
-      int b, h, ci;
-      decode_chunk(bt, c, b, h, ci);
-      const int valid = min(chunk, bt.s[b].n - ci * chunk);
-      const int ntiles = (valid + kTileKeys - 1) / kTileKeys;
-      float run[G];
-      int cnt[G];
-#pragma unroll
-      for (int j = 0; j < G; ++j) {
-        run[j] = dec_max(ws.gmax[b * bt.Hq + h * G + j]);  // any real max is a valid bound
-        cnt[j] = 0;
-      }
-      const size_t cbase = (size_t)c * G;
-      for (int tl = 0; tl < ntiles; ++tl, ++tcount) {
-        mbar_wait(accf_bar(acc), aphase);
-        fence_after();
-        float v[NP];
-        tmem_ld<NP>(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NP, v);
-        fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(acce_bar(acc));
-        if (++acc == 2) { acc = 0; aphase ^= 1; }
-
-        const int row = tl * kTileKeys + quarter * 32 + lane;
-        const bool ok = row < valid;
-        float sc[G];
-        const int tb = tcount & 1;
-#pragma unroll
-        for (int j = 0; j < G; ++j) {
-          sc[j] = ok ? v[j] + (v[G + j] + v[2 * G + j]) : -INFINITY;
-          const float m = warp_max(sc[j]);
-          if (lane == 0) tmax[(tb * 4 + quarter) * G + j] = m;
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        unsigned bal[G];
-#pragma unroll
-        for (int j = 0; j < G; ++j) {
-          float tm = tmax[(tb * 4 + 0) * G + j];
-#pragma unroll
-          for (int qq = 1; qq < 4; ++qq) tm = fmaxf(tm, tmax[(tb * 4 + qq) * G + j]);
-          run[j] = fmaxf(run[j], tm);
-          const bool pass = ok && sc[j] >= run[j] - bt.beta;
-          bal[j] = __ballot_sync(kFull, pass);
-          if (lane == 0) wcnt[(tb * 4 + quarter) * G + j] = __popc(bal[j]);
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-#pragma unroll
-        for (int j = 0; j < G; ++j) {
-          int off = cnt[j], tot = 0;
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) {
-            const int w = wcnt[(tb * 4 + qq) * G + j];
-            off += qq < quarter ? w : 0;
-            tot += w;
-          }
-          if ((bal[j] >> lane) & 1u) {
-            const int o = off + __popc(bal[j] & lanemask_lt());
-            ws.cidx[(cbase + j) * chunk + o] = row;
-            ws.cscore[(cbase + j) * chunk + o] = sc[j];
-          }
-          cnt[j] += tot;
-        }
-      }
-      // publish the chunk's max and candidate counts (identical in every thread)
-      const int et = threadIdx.x - 64;
-      if (et < G) {
-#pragma unroll
-        for (int j = 0; j < G; ++j) {
-          if (j == et) {
-            atomicMax(&ws.gmax[b * bt.Hq + h * G + j], enc_max(run[j]));
-            ws.cnt[cbase + j] = cnt[j];
-          }
-        }
-      }
+      int b, h;
+      epilogue_chunk<G, NP>(bt, ws, c, quarter, lane, tmem_base, accf0, acce0, acc, aphase, b, h);
     }
   }
   fence_before();
   __syncthreads();
   if (warp == 1) {
     fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * NP));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kAcc * NP));
   }
 }
 
 inline size_t tc_smem_bytes(int G, int kStages) {
   const int NP = (3 * G <= 16) ? 16 : 32;
-  return 1024 + (size_t)kStages * kTileBytes + 2 * 2 * NP * 128 + 8 * (2 * kStages + 4) + 16 +
-         2 * 4 * G * 8 + 64;
+  return 1024 + (size_t)kStages * kTileBytes + 2 * 2 * NP * 128 + 8 * (2 * kStages + 2 * kAcc) + 64;
 }
 
 }  // namespace tc

@@ -7,6 +7,7 @@
 #include <mutex>
 
 #include "alaya_dispatch.cuh"
+#include "alaya_fused.cuh"
 #include "alaya_tc.cuh"
 
 namespace alaya {
@@ -26,6 +27,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+}  // namespace
+
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -37,48 +40,39 @@ int num_sms() {
   return n;
 }
 
+namespace {
+
 int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
   return v && *v ? atoi(v) : dflt;
 }
 
 template <int G, int S>
-int launch_s(const Batch& bt, const tc::Maps& maps, const float* q, const Ws& ws, cudaStream_t st) {
+int launch_s(const Batch& bt, const tc::Maps& maps, const float* q, const Ws& ws, cudaStream_t st,
+             int ctas_per_sm) {
   const size_t sm = tc::tc_smem_bytes(G, S);
   cudaFuncSetAttribute(tc::scan_tc_kernel<G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  const int grid = std::min(bt.total_chunks, num_sms());
+  const int grid = std::min(bt.total_chunks, ctas_per_sm * num_sms());
   tc::scan_tc_kernel<G, S><<<grid, tc::kThreadsTc, sm, st>>>(bt, maps, q, ws);
   return cuda_check("scan_tc_kernel");
 }
 
-// pipeline depth: ALAYA_TC_STAGES (4..6) overrides the default of 6
+// Persistent CTAs per SM (ALAYA_TC_CTAS, default 3): 2 CTAs with 3-stage rings
+// or 3 CTAs with 2-stage rings overlap their TMA->MMA->epilogue handshakes;
+// 1 CTA uses ALAYA_TC_STAGES (4..6, default 6).
 template <int G>
 int launch(const Batch& bt, const tc::Maps& maps, const float* q, const Ws& ws, cudaStream_t st) {
+  static const int ctas = env_int("ALAYA_TC_CTAS", 3);
   static const int stages = env_int("ALAYA_TC_STAGES", 6);
-  if (stages <= 4) return launch_s<G, 4>(bt, maps, q, ws, st);
-  if (stages == 5) return launch_s<G, 5>(bt, maps, q, ws, st);
-  return launch_s<G, 6>(bt, maps, q, ws, st);
+  if (ctas >= 3) return launch_s<G, 2>(bt, maps, q, ws, st, 3);
+  if (ctas == 2) return launch_s<G, 3>(bt, maps, q, ws, st, 2);
+  if (stages <= 4) return launch_s<G, 4>(bt, maps, q, ws, st, 1);
+  if (stages == 5) return launch_s<G, 5>(bt, maps, q, ws, st, 1);
+  return launch_s<G, 6>(bt, maps, q, ws, st, 1);
 }
 
-}  // namespace
-
-bool tc_scan_eligible(const Batch& bt, int dtype, const alaya_seq* seqs) {
-  if (dtype != ALAYA_BF16 || bt.D != 128 || bt.G > 8 || bt.chunk % tc::kTileKeys) return false;
-  int distinct = 0;
-  for (int b = 0; b < bt.B; ++b) {
-    if (seqs[b].n == 0) continue;
-    if (seqs[b].head_stride % 128 || reinterpret_cast<uintptr_t>(seqs[b].k) % 16) return false;
-    bool seen = false;
-    for (int a = 0; a < b && !seen; ++a) seen = seqs[a].k == seqs[b].k;
-    distinct += !seen;
-  }
-  return distinct <= tc::kMaxMaps && encode_fn() != nullptr;
-}
-
-int launch_tc_scan(const Batch& bt, const alaya_seq* seqs, const float* q, const Ws& ws,
-                   cudaStream_t st) {
-  if (bt.total_chunks == 0) return ALAYA_OK;
-  static thread_local tc::Maps maps;  // ~19 KB: keep off the stack
+// One TMA tensor map per distinct K slab (sessions sharing a context share it).
+int build_maps(const Batch& bt, const alaya_seq* seqs, tc::Maps& maps) {
   auto enc = encode_fn();
   // L2 sector promotion of the K boxes: ALAYA_TC_PROMO 0..3 = none/64B/128B/256B
   static const CUtensorMapL2promotion promo =
@@ -100,11 +94,74 @@ int launch_tc_scan(const Batch& bt, const alaya_seq* seqs, const float* q, const
     cuuint32_t estride[2] = {1, 1};
     CUresult r = enc(&maps.m[nmaps], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(seqs[b].k),
                      gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_128B, promo,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     CU_TENSOR_MAP_SWIZZLE_128B, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(ALAYA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     maps.map_of_seq[b] = (int16_t)nmaps++;
   }
+  return ALAYA_OK;
+}
+
+template <int G, int S>
+int launch_fused_s(const Batch& bt, const tc::Maps& maps, const float* q, const Ws& ws, cudaStream_t st) {
+  const size_t sm = fused::fused_smem_bytes(G, S);
+  cudaFuncSetAttribute(fused::fused_tc_kernel<G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  fused::fused_tc_kernel<G, S><<<num_sms(), fused::kThreadsFused, sm, st>>>(bt, maps, q, ws, ws.group_done);
+  return cuda_check("fused_tc_kernel");
+}
+
+template <int G>
+int launch_fused(const Batch& bt, const tc::Maps& maps, const float* q, const Ws& ws, cudaStream_t st) {
+  static const int stages = env_int("ALAYA_TC_STAGES", 5);
+  if (stages <= 4) return launch_fused_s<G, 4>(bt, maps, q, ws, st);
+  return launch_fused_s<G, 5>(bt, maps, q, ws, st);
+}
+
+}  // namespace
+
+bool tc_scan_eligible(const Batch& bt, int dtype, const alaya_seq* seqs) {
+  if (dtype != ALAYA_BF16 || bt.D != 128 || bt.G > 8 || bt.chunk % (4 * tc::kTileKeys)) return false;
+  int distinct = 0;
+  for (int b = 0; b < bt.B; ++b) {
+    if (seqs[b].n == 0) continue;
+    if (seqs[b].head_stride % 128 || reinterpret_cast<uintptr_t>(seqs[b].k) % 16) return false;
+    bool seen = false;
+    for (int a = 0; a < b && !seen; ++a) seen = seqs[a].k == seqs[b].k;
+    distinct += !seen;
+  }
+  return distinct <= tc::kMaxMaps && encode_fn() != nullptr;
+}
+
+bool fused_enabled() {
+  static const int on = env_int("ALAYA_FUSED", 0);
+  return on != 0;
+}
+
+int launch_tc_fused(const Batch& bt, const alaya_seq* seqs, const float* q, const Ws& ws,
+                    cudaStream_t st) {
+  static thread_local tc::Maps maps;
+  int rc = build_maps(bt, seqs, maps);
+  if (rc) return rc;
+  switch (bt.G) {
+    case 1: return launch_fused<1>(bt, maps, q, ws, st);
+    case 2: return launch_fused<2>(bt, maps, q, ws, st);
+    case 3: return launch_fused<3>(bt, maps, q, ws, st);
+    case 4: return launch_fused<4>(bt, maps, q, ws, st);
+    case 5: return launch_fused<5>(bt, maps, q, ws, st);
+    case 6: return launch_fused<6>(bt, maps, q, ws, st);
+    case 7: return launch_fused<7>(bt, maps, q, ws, st);
+    default: return launch_fused<8>(bt, maps, q, ws, st);
+  }
+}
+
+int launch_tc_scan(const Batch& bt_in, const alaya_seq* seqs, const float* q, const Ws& ws,
+                   cudaStream_t st) {
+  if (bt_in.total_chunks == 0) return ALAYA_OK;
+  static thread_local Batch bt;
+  bt = bt_in;
+  bt.dbg = env_int("ALAYA_TC_DBG", 0);
+  static thread_local tc::Maps maps;  // ~19 KB: keep off the stack
+  int rc = build_maps(bt, seqs, maps);
+  if (rc) return rc;
   switch (bt.G) {
     case 1: return launch<1>(bt, maps, q, ws, st);
     case 2: return launch<2>(bt, maps, q, ws, st);
