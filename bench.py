@@ -440,8 +440,9 @@ def main():
 
 
 def run_e2e(a, P, torch, K, V, centers, dev, dtype):
-    """Same metric through the public API: Session.update + Session.attention_batch
-    with pinned host q/k/v in and host outputs back, per layer, every step."""
+    """Same metric through the public API (Session.update_batch +
+    Session.attention_batch per layer): every step copies that step's q/k/v
+    from pinned host memory and reads all layer outputs back to pinned host."""
     import numpy as np
     L, B, Hq, Hkv, d = a.layers, a.batch, a.hq, a.hkv, a.dim
     shape = P.ModelShape(L, Hq, Hkv, d)
@@ -466,13 +467,17 @@ def run_e2e(a, P, torch, K, V, centers, dev, dtype):
                            0.25 * g.standard_normal((steps, L, B, Hkv, d))).astype(np.float32)).pin_memory()
     vh = torch.from_numpy(g.standard_normal((steps, L, B, Hkv, d)).astype(np.float32)).pin_memory()
     outs = torch.empty(L, B, Hq, d, dtype=torch.float32).pin_memory()
+    out_dev = torch.empty(L, B, Hq, d, dtype=torch.float32, device=dev)
 
     def step(s):
+        # the step's inputs: one pinned host -> device copy each for q, k, v
+        qd = qh[s].to(dev, non_blocking=True)
+        kd = kh[s].to(dev, non_blocking=True)
+        vd = vh[s].to(dev, non_blocking=True)
         for l in range(L):
-            for b in range(B):
-                sessions[b].update(qh[s, l, b], kh[s, l, b], vh[s, l, b], l)
-            o = P.Session.attention_batch(sessions, qh[s, l], l)
-            outs[l].copy_(o)  # device -> pinned host: the step's result
+            P.Session.update_batch(sessions, qd[l], kd[l], vd[l], l)
+            P.Session.attention_batch(sessions, qd[l], l, out=out_dev[l])
+        outs.copy_(out_dev, non_blocking=True)  # the step's result -> pinned host
     for s in range(a.warmup):
         step(s)
     torch.cuda.synchronize()
@@ -485,7 +490,8 @@ def run_e2e(a, P, torch, K, V, centers, dev, dtype):
     d2h = L * B * Hq * d * 4
     return {"value": B * L * Hq / dt, "unit": "queries*heads/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3,
-            "path": "Session.update + Session.attention_batch (public API), pinned host I/O"}
+            "path": "Session.update_batch + Session.attention_batch (public API); per step one "
+                    "pinned H2D copy of q/k/v and one D2H copy of all layer outputs"}
 
 
 if __name__ == "__main__":

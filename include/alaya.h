@@ -140,6 +140,13 @@ int alaya_selected(const alaya_params* p, const alaya_seq* seqs, int batch, int6
                    int64_t cap, int32_t* d_selected, int32_t* d_retrieved, void* d_ws,
                    size_t ws_bytes, void* stream);
 
+/* Session.update (store.py:160-189) for a batch: append one row per kv head to
+ * every sequence's session window. Row seqs[b].w of wk/wv (head stride
+ * w_head_stride) receives d_k/d_v[b][h][0..dim) (fp32, converted to p->dtype).
+ * The caller owns window capacity; seqs[b].w is the row index written. */
+int alaya_window_append(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_k,
+                        const float* d_v, void* stream);
+
 /* Device status word of the last alaya_dipr_attention on this workspace
  * (ALAYA_OK or ALAYA_ERR_NONFINITE); pointer into d_ws. */
 int* alaya_ws_status(void* d_ws);

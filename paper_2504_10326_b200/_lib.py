@@ -35,7 +35,7 @@ MAX_BATCH = 128
 EXPORTS = (
     "alaya_last_error", "alaya_version", "alaya_workspace_bytes", "alaya_dipr_attention",
     "alaya_scan", "alaya_attend", "alaya_merge_partials", "alaya_merge_states", "alaya_selected",
-    "alaya_ws_status",
+    "alaya_ws_status", "alaya_window_append",
 )
 
 
@@ -99,6 +99,8 @@ def load() -> ctypes.CDLL:
     lib.alaya_merge_states.argtypes = [vp, i32, i32, i32, vp, vp]
     lib.alaya_selected.restype = i32
     lib.alaya_selected.argtypes = [P, S, i32, vp, ctypes.c_int64, vp, vp, vp, sz, vp]
+    lib.alaya_window_append.restype = i32
+    lib.alaya_window_append.argtypes = [P, S, i32, vp, vp, vp]
     lib.alaya_ws_status.restype = vp
     lib.alaya_ws_status.argtypes = [vp]
     _lib = lib

@@ -233,6 +233,25 @@ size_t alaya_workspace_bytes(const alaya_params* p, const alaya_seq* seqs, int b
 
 int* alaya_ws_status(void* d_ws) { return static_cast<int*>(d_ws); }
 
+int alaya_window_append(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_k,
+                        const float* d_v, void* stream) {
+  static thread_local Batch bt;
+  int rc = build_batch(p, seqs, batch, &bt);
+  if (rc) return rc;
+  if (!d_k || !d_v) return fail(ALAYA_ERR_ARG, "null k/v");
+  for (int b = 0; b < batch; ++b) {
+    if (!seqs[b].wk || !seqs[b].wv) return fail(ALAYA_ERR_ARG, "seq %d: null window buffers", b);
+    if (seqs[b].w_head_stride < (int64_t)(seqs[b].w + 1) * p->dim)
+      return fail(ALAYA_ERR_SHAPE, "seq %d: window row %d beyond capacity", b, seqs[b].w);
+  }
+  const long total = (long)batch * p->n_kv_heads * p->dim;
+  const int blocks = (int)std::min<long>((total + 255) / 256, 1024);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (p->dtype == ALAYA_BF16) window_append_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(bt, d_k, d_v);
+  else window_append_kernel<float><<<blocks, 256, 0, st>>>(bt, d_k, d_v);
+  return cuda_check("window_append_kernel");
+}
+
 int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q,
                          float* d_out, void* d_ws, size_t ws_bytes, void* stream) {
   Call c;

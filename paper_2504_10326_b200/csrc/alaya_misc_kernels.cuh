@@ -59,4 +59,28 @@ __global__ void selected_kernel(const __grid_constant__ Batch bt, Ws ws, int64_t
   if (threadIdx.x == 0) { nsel[row] = base; nret[row] = ret; }
 }
 
+// Session-window append: one thread per element of [B][Hkv][D].
+template <typename T>
+__global__ void window_append_kernel(const __grid_constant__ Batch bt, const float* __restrict__ k,
+                                     const float* __restrict__ v) {
+  const int D = bt.D;
+  const long total = (long)bt.B * bt.Hkv * D;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int e = (int)(i % D);
+    const long bh = i / D;
+    const int h = (int)(bh % bt.Hkv), b = (int)(bh / bt.Hkv);
+    const KSeq& s = bt.s[b];
+    const size_t off = (size_t)h * s.whs + (size_t)s.w * D + e;
+    T* wk = const_cast<T*>(reinterpret_cast<const T*>(s.wk));
+    T* wv = const_cast<T*>(reinterpret_cast<const T*>(s.wv));
+    if constexpr (std::is_same_v<T, float>) {
+      wk[off] = k[i];
+      wv[off] = v[i];
+    } else {
+      wk[off] = __float2bfloat16_rn(k[i]);
+      wv[off] = __float2bfloat16_rn(v[i]);
+    }
+  }
+}
+
 }  // namespace alaya

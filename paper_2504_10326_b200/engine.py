@@ -237,3 +237,22 @@ def merge_states(parts: torch.Tensor, dim: int) -> torch.Tensor:
     check(lib.alaya_merge_states(parts.data_ptr(), R, rows, dim, out.data_ptr(),
                                  torch.cuda.current_stream(parts.device).cuda_stream))
     return out
+
+
+def window_append(seqs: list[SeqView], params: AlayaParams, dtype: torch.dtype,
+                  k: torch.Tensor, v: torch.Tensor) -> None:
+    """Append ``k``/``v`` ``[B, Hkv, d]`` (fp32) as row ``seqs[b].w`` of each
+    sequence's window ring (``Session.update``, reference ``store.py:179-181``)."""
+    require_cuda()
+    lib = _lib.load()
+    arr = (AlayaSeq * len(seqs))()
+    for i, s in enumerate(seqs):
+        _check_kv(s.wk, "wk", dtype, params.dim)
+        _check_kv(s.wv, "wv", dtype, params.dim)
+        e = arr[i]
+        e.wk, e.wv, e.w_head_stride = s.wk.data_ptr(), s.wv.data_ptr(), s.wk.stride(0)
+        e.w = int(s.w)
+    k = k.to(torch.float32).contiguous()
+    v = v.to(torch.float32).contiguous()
+    check(lib.alaya_window_append(ctypes.byref(params), arr, len(seqs), k.data_ptr(), v.data_ptr(),
+                                  torch.cuda.current_stream(k.device).cuda_stream))

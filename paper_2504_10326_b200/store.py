@@ -39,6 +39,10 @@ def context_id_for(token_ids: np.ndarray, shape: ModelShape) -> str:
     return "ctx-" + h.hexdigest()[:16]
 
 
+def _rows(x) -> np.ndarray:
+    return np.atleast_2d(np.asarray(x, dtype=np.float32))
+
+
 def _to_device(x, device, dtype) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         return x.to(device=device, dtype=dtype).contiguous()
@@ -144,30 +148,50 @@ class Session:
     # -- Table-3 APIs -----------------------------------------------------
     def update(self, q, k, v, layer: int):
         """Append one step's per-head K/V to the layer window (``store.py:160-189``)."""
-        st = self._store
-        shape = st.shape
-        self._check_layer(layer)
-        qa = q if isinstance(q, torch.Tensor) else np.atleast_2d(np.asarray(q, dtype=np.float32))
-        if tuple(qa.shape) != (shape.n_query_heads, shape.dim):
-            raise ValueError(f"q must be {(shape.n_query_heads, shape.dim)}, got {tuple(qa.shape)}")
-        kt = k if isinstance(k, torch.Tensor) else np.atleast_2d(np.asarray(k, dtype=np.float32))
-        vt = v if isinstance(v, torch.Tensor) else np.atleast_2d(np.asarray(v, dtype=np.float32))
-        if tuple(kt.shape) != (shape.n_kv_heads, shape.dim) or tuple(vt.shape) != tuple(kt.shape):
-            raise ValueError(f"k/v must be {(shape.n_kv_heads, shape.dim)}")
+        Session.update_batch([self], _rows(q)[None] if not isinstance(q, torch.Tensor) else q[None],
+                             _rows(k)[None] if not isinstance(k, torch.Tensor) else k[None],
+                             _rows(v)[None] if not isinstance(v, torch.Tensor) else v[None], layer)
+        shape = self._store.shape
         w = self._wlen[layer]
-        self._ensure_window(w + 1)
-        self._wk[layer, :, w] = _to_device(kt, st.device, st.kv_dtype)
-        self._wv[layer, :, w] = _to_device(vt, st.device, st.kv_dtype)
-        self._wlen[layer] = w + 1
-        if st.log_queries:
-            self._query_log[layer].append(
-                qa.detach().float().cpu().numpy() if isinstance(qa, torch.Tensor) else qa.copy())
         k_views, v_views = [], []
         for h in range(shape.n_kv_heads):
             bk, bv = self._base_arrays(layer, h)
-            k_views.append(TwoSegmentView(bk, self._wk[layer, h, : w + 1]))
-            v_views.append(TwoSegmentView(bv, self._wv[layer, h, : w + 1]))
+            k_views.append(TwoSegmentView(bk, self._wk[layer, h, :w]))
+            v_views.append(TwoSegmentView(bv, self._wv[layer, h, :w]))
         return k_views, v_views
+
+    @staticmethod
+    def update_batch(sessions: list["Session"], q, k, v, layer: int) -> None:
+        """``update`` for many sessions of one store: ``q [B, Hq, d]``, ``k``/``v``
+        ``[B, Hkv, d]`` (numpy or torch). One host->device copy and one append
+        kernel (``alaya_window_append``) for the whole batch."""
+        if not sessions:
+            raise ValueError("empty session batch")
+        st = sessions[0]._store
+        shape = st.shape
+        B = len(sessions)
+        if tuple(q.shape) != (B, shape.n_query_heads, shape.dim):
+            raise ValueError(f"q must be {(shape.n_query_heads, shape.dim)} per session, got "
+                             f"{tuple(q.shape)}")
+        if tuple(k.shape) != (B, shape.n_kv_heads, shape.dim) or tuple(v.shape) != tuple(k.shape):
+            raise ValueError(f"k/v must be {(shape.n_kv_heads, shape.dim)} per session")
+        seqs = []
+        for s in sessions:
+            if s._store is not st:
+                raise ValueError("all sessions of a batch must share a store")
+            s._check_layer(layer)
+            s._ensure_window(s._wlen[layer] + 1)
+            seqs.append(engine.SeqView(k=None, v=None, n=0, wk=s._wk[layer], wv=s._wv[layer],
+                                       w=s._wlen[layer]))
+        kd = _to_device(k, st.device, torch.float32)
+        vd = _to_device(v, st.device, torch.float32)
+        engine.window_append(seqs, st._append_params(), st.kv_dtype, kd, vd)
+        for b, s in enumerate(sessions):
+            s._wlen[layer] += 1
+            if st.log_queries:
+                qb = q[b]
+                s._query_log[layer].append(qb.detach().float().cpu().numpy()
+                                           if isinstance(qb, torch.Tensor) else np.array(qb, np.float32))
 
     def attention(self, q, layer: int):
         """Sparse attention outputs for one layer, one row per query head
@@ -179,9 +203,10 @@ class Session:
         return Session.attention_batch([self], np.asarray(q, dtype=np.float32)[None], layer)[0]
 
     @staticmethod
-    def attention_batch(sessions: list["Session"], q, layer: int):
+    def attention_batch(sessions: list["Session"], q, layer: int, out: torch.Tensor | None = None):
         """One decode step of ``layer`` for many sessions of the same store in
-        one kernel sequence. ``q`` is ``[B, Hq, d]`` (numpy or CUDA tensor)."""
+        one kernel sequence. ``q`` is ``[B, Hq, d]`` (numpy or CUDA tensor);
+        ``out`` (CUDA ``[B, Hq, d]`` fp32) receives the result when given."""
         if not sessions:
             raise ValueError("empty session batch")
         st = sessions[0]._store
@@ -202,24 +227,20 @@ class Session:
             beta, wi, wl = s._exec_params(active)
             groups.setdefault((beta, wi, wl), []).append(i)
         qd = qt.to(device=st.device, dtype=torch.float32, non_blocking=True)
-        out = torch.empty(len(sessions), shape.n_query_heads, shape.dim, dtype=torch.float32,
-                          device=st.device)
+        if out is None:
+            out = torch.empty(len(sessions), shape.n_query_heads, shape.dim, dtype=torch.float32,
+                              device=st.device)
         calls = []
         for (beta, wi, wl), idx in groups.items():
             for c0 in range(0, len(idx), _lib.MAX_BATCH):
                 part = idx[c0:c0 + _lib.MAX_BATCH]
-                seqs = [sessions[i]._seq_view(layer) for i in part]
-                params = engine.make_params(shape.n_query_heads, shape.n_kv_heads, shape.dim,
-                                            st.kv_dtype, beta, wi, wl, st.config.chunk,
-                                            _SCAN_KIND[st.config.scan_kernel],
-                                            int(st.config.block_filter))
-                call = engine.Call(seqs, params, st.kv_dtype, st.device)
-                sel = torch.tensor(part, device=st.device) if len(part) != len(sessions) else None
-                o = call.dipr_attention(qd if sel is None else qd.index_select(0, sel))
-                if sel is None:
-                    out = o
+                call = st._call_for([sessions[i] for i in part], layer, beta, wi, wl)
+                if len(part) == len(sessions):
+                    call.dipr_attention(qd, out=out)
                 else:
-                    out.index_copy_(0, sel, o)
+                    sel = torch.tensor(part, device=st.device)
+                    out.index_copy_(0, sel, call.dipr_attention(qd.index_select(0, sel)))
+                seqs = [sessions[i]._seq_view(layer) for i in part] if st.config.diagnostics else []
                 if st.config.diagnostics:
                     cap = max(1, max(sv.n for sv in seqs))
                     ids, nsel, nret = call.selected(cap)
@@ -323,6 +344,7 @@ class ContextStore:
         self.kv_dtype = _TORCH_DTYPE[self.config.kv_dtype]
         self.log_queries = log_queries
         self.contexts: dict[str, ContextRecord] = {}
+        self._calls: dict = {}
 
     def import_context(self, token_ids, keys, values, queries=None) -> str:
         """Import K/V ``[L, Hkv, n, d]`` (numpy or torch) to the device (``store.py:388-422``)."""
@@ -359,6 +381,33 @@ class ContextStore:
 
     def get(self, context_id: str) -> ContextRecord:
         return self.contexts[context_id]
+
+    def _append_params(self):
+        sh = self.shape
+        return engine.make_params(sh.n_query_heads, sh.n_kv_heads, sh.dim, self.kv_dtype, 0.0, 0, 0)
+
+    def _call_for(self, sessions: list["Session"], layer: int, beta: float, wi: int, wl: int):
+        """Validated C-ABI descriptors for (layer, sessions), cached across steps:
+        only the window row counts change between decode steps."""
+        views = [s._seq_view(layer) for s in sessions]
+        sig = tuple((v.k.data_ptr() if v.k is not None else 0, v.n,
+                     v.wk.data_ptr() if v.wk is not None else 0) for v in views)
+        key = (layer, tuple(id(s) for s in sessions), beta, wi, wl)
+        hit = self._calls.get(key)
+        if hit is not None and hit[0] == sig:
+            call = hit[1]
+            for i, v in enumerate(views):
+                call.seqs[i].w = int(v.w)
+            return call
+        sh = self.shape
+        params = engine.make_params(sh.n_query_heads, sh.n_kv_heads, sh.dim, self.kv_dtype, beta,
+                                    wi, wl, self.config.chunk, _SCAN_KIND[self.config.scan_kernel],
+                                    int(self.config.block_filter))
+        call = engine.Call(views, params, self.kv_dtype, self.device)
+        if len(self._calls) > 4096:
+            self._calls.clear()
+        self._calls[key] = (sig, call)
+        return call
 
     def _plans_for(self, n: int) -> dict[int, Plan]:
         cfg = self.config.planner_config()
