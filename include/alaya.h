@@ -75,6 +75,12 @@ typedef struct {
   int64_t prefix_len;
   int32_t n;
   int32_t w;
+  /* Coarse block filter input (alaya_block_bounds output for this layer slab):
+   * [Hkv][bounds_head_stride elements], per 128-token block [5][dim] in the K
+   * dtype: min, max, mean, representative key, radius. NULL when
+   * params.block_filter == 0. */
+  const void* bounds;
+  int64_t bounds_head_stride;
 } alaya_seq;
 
 typedef struct {
@@ -87,7 +93,10 @@ typedef struct {
   int32_t win_last;      /* WindowConfig.last (core.py:153) */
   int32_t chunk;         /* tokens per work chunk; 0 = auto */
   int32_t scan_kind;     /* alaya_scan_kind */
-  int32_t block_filter;  /* 1 = skip blocks with a sound UB < LB - beta */
+  int32_t block_filter;  /* 1 = skip 128-token blocks whose sound upper bound
+                          * sum_d max(q_d lo_d, q_d hi_d) is below LB - beta, LB
+                          * = max score of the base-window tokens (a lower bound
+                          * of the DIPR max). Exact: the DIPR set is unchanged. */
 } alaya_params;
 
 #define ALAYA_MAX_BATCH 128
@@ -146,6 +155,21 @@ int alaya_selected(const alaya_params* p, const alaya_seq* seqs, int batch, int6
  * The caller owns window capacity; seqs[b].w is the row index written. */
 int alaya_window_append(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_k,
                         const float* d_v, void* stream);
+
+/* Coarse block index build (input of the block filter; the reference's
+ * BlockIndex, index.py:195-243, ranks blocks by representatives -- a heuristic
+ * -- while a filter that must keep the exact DIPR set needs a sound bound):
+ * per kv head h and 128-token block i of d_k ([heads][head_stride] elements,
+ * n rows), d_bounds[h*bounds_head_stride + i*5*dim + r*dim + e] with rows
+ * r = 0 min, 1 max, 2 mean, 3 largest-norm key (the reference's
+ * representative, index.py:217-228), 4 [e=0] radius max||k - mean|| (rounded up).
+ * bounds_head_stride >= ceil(n/128)*5*dim. */
+int alaya_block_bounds(const void* d_k, int dtype, int n_heads, int64_t head_stride, int n, int dim,
+                       void* d_bounds, int64_t bounds_head_stride, void* stream);
+
+/* Blocks kept / blocks considered by the block filter in the last scan on
+ * this workspace: device pointer to two int32 (valid after the scan). */
+int* alaya_ws_block_stats(const alaya_params* p, const alaya_seq* seqs, int batch, void* d_ws);
 
 /* Device status word of the last alaya_dipr_attention on this workspace
  * (ALAYA_OK or ALAYA_ERR_NONFINITE); pointer into d_ws. */

@@ -35,7 +35,7 @@ MAX_BATCH = 128
 EXPORTS = (
     "alaya_last_error", "alaya_version", "alaya_workspace_bytes", "alaya_dipr_attention",
     "alaya_scan", "alaya_attend", "alaya_merge_partials", "alaya_merge_states", "alaya_selected",
-    "alaya_ws_status", "alaya_window_append",
+    "alaya_ws_status", "alaya_window_append", "alaya_block_bounds", "alaya_ws_block_stats",
 )
 
 
@@ -48,6 +48,7 @@ class AlayaSeq(ctypes.Structure):
         ("head_stride", ctypes.c_int64), ("w_head_stride", ctypes.c_int64),
         ("token_offset", ctypes.c_int64), ("prefix_len", ctypes.c_int64),
         ("n", ctypes.c_int32), ("w", ctypes.c_int32),
+        ("bounds", ctypes.c_void_p), ("bounds_head_stride", ctypes.c_int64),
     ]
 
 
@@ -101,6 +102,10 @@ def load() -> ctypes.CDLL:
     lib.alaya_selected.argtypes = [P, S, i32, vp, ctypes.c_int64, vp, vp, vp, sz, vp]
     lib.alaya_window_append.restype = i32
     lib.alaya_window_append.argtypes = [P, S, i32, vp, vp, vp]
+    lib.alaya_block_bounds.restype = i32
+    lib.alaya_block_bounds.argtypes = [vp, i32, i32, ctypes.c_int64, i32, i32, vp, ctypes.c_int64, vp]
+    lib.alaya_ws_block_stats.restype = vp
+    lib.alaya_ws_block_stats.argtypes = [P, S, i32, vp]
     lib.alaya_ws_status.restype = vp
     lib.alaya_ws_status.argtypes = [vp]
     _lib = lib

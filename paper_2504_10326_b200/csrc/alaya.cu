@@ -73,6 +73,9 @@ int build_batch(const alaya_params* p, const alaya_seq* seqs, int B, Batch* bt) 
       return fail(ALAYA_ERR_SHAPE, "seq %d: head_stride too small", b);
     if (s.w > 0 && s.w_head_stride < (int64_t)s.w * p->dim)
       return fail(ALAYA_ERR_SHAPE, "seq %d: w_head_stride too small", b);
+    if (p->block_filter && s.n > 0 &&
+        (!s.bounds || s.bounds_head_stride < (int64_t)((s.n + 127) / 128) * 5 * p->dim))
+      return fail(ALAYA_ERR_ARG, "seq %d: block_filter needs bounds (alaya_block_bounds)", b);
     tokens += s.n;
     if (s.n > maxn) maxn = s.n;
   }
@@ -101,6 +104,7 @@ int build_batch(const alaya_params* p, const alaya_seq* seqs, int B, Batch* bt) 
   bt->wi = p->win_initial;
   bt->wl = p->win_last;
   bt->inv_sqrt_d = (float)(1.0 / std::sqrt((double)p->dim));
+  bt->block_filter = p->block_filter ? 1 : 0;
   int cb = 0;
   for (int b = 0; b < B; ++b) {
     const alaya_seq& s = seqs[b];
@@ -110,6 +114,8 @@ int build_batch(const alaya_params* p, const alaya_seq* seqs, int B, Batch* bt) 
     k.off = s.token_offset; k.P = s.prefix_len;
     k.n = s.n; k.w = s.w;
     k.nch = (s.n + chunk - 1) / chunk;
+    k.bnd = s.bounds;
+    k.bhs = s.bounds_head_stride;
     k.chunk_base = cb;
     cb += p->n_kv_heads * k.nch;
   }
@@ -122,7 +128,7 @@ size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 struct Layout {
   size_t zero_bytes;
   size_t status, gmax, counters, cnt, selcnt, retcnt, part_l, part_acc, cidx, cscore, partbuf, smaxbuf,
-      bfkeep, total;
+      keep, lbu, total;
 };
 
 Layout layout_for(const Batch& bt) {
@@ -131,7 +137,8 @@ Layout layout_for(const Batch& bt) {
   size_t o = 0;
   L.status = o; o = align_up(o + 4);
   L.gmax = o; L.counters = o + 4 * rows;
-  L.zero_bytes = 4 * rows + 64 + 4 * (size_t)bt.B * bt.Hkv;  // gmax + counters + group_done
+  L.lbu = L.counters + 64 + 4 * (size_t)bt.B * bt.Hkv;
+  L.zero_bytes = 4 * rows + 64 + 4 * (size_t)bt.B * bt.Hkv + 4 * rows;  // gmax, counters, group_done, lbu
   o = align_up(o + L.zero_bytes);
   L.cnt = o; o = align_up(o + 4 * C * G * 4);
   L.selcnt = o; o = align_up(o + 4 * C * G);
@@ -142,7 +149,7 @@ Layout layout_for(const Batch& bt) {
   L.cscore = o; o = align_up(o + 4 * C * G * bt.chunk);
   L.partbuf = o; o = align_up(o + 4 * rows * (D + 2));
   L.smaxbuf = o; o = align_up(o + 4 * rows);
-  L.bfkeep = o; o = align_up(o + 4 * C);
+  L.keep = o; o = align_up(o + 8 * C);
   L.total = o;
   return L;
 }
@@ -163,7 +170,8 @@ Ws carve(const Layout& L, void* base) {
   w.cscore = reinterpret_cast<float*>(c + L.cscore);
   w.partbuf = reinterpret_cast<float*>(c + L.partbuf);
   w.smaxbuf = reinterpret_cast<float*>(c + L.smaxbuf);
-  w.bfkeep = reinterpret_cast<int*>(c + L.bfkeep);
+  w.keep = reinterpret_cast<unsigned long long*>(c + L.keep);
+  w.lbu = reinterpret_cast<uint32_t*>(c + L.lbu);
   return w;
 }
 
@@ -212,6 +220,10 @@ int run_scan(Call& c, const float* d_q) {
   const size_t rows = (size_t)c.bt.B * c.bt.Hq;
   (void)rows;
   if (cudaMemsetAsync(c.ws.gmax, 0, c.L.zero_bytes, c.stream) != cudaSuccess) return cuda_check("memset");
+  if (c.bt.block_filter) {
+    const int rc = c.st.filter(c.bt, d_q, c.ws, c.stream);
+    if (rc) return rc;
+  }
   if (c.use_tc) return launch_tc_scan(c.bt, c.seqs, d_q, c.ws, c.stream);
   return c.st.scan(c.bt, d_q, c.ws, c.stream);
 }
@@ -232,6 +244,34 @@ size_t alaya_workspace_bytes(const alaya_params* p, const alaya_seq* seqs, int b
 }
 
 int* alaya_ws_status(void* d_ws) { return static_cast<int*>(d_ws); }
+
+int alaya_block_bounds(const void* d_k, int dtype, int n_heads, int64_t head_stride, int n, int dim,
+                       void* d_bounds, int64_t bounds_head_stride, void* stream) {
+  if (!d_k || !d_bounds || n_heads < 1 || n < 0 || !dim_ok(dim))
+    return fail(ALAYA_ERR_ARG, "bad block bounds arguments");
+  if (head_stride < (int64_t)n * dim || bounds_head_stride < (int64_t)((n + 127) / 128) * 5 * dim)
+    return fail(ALAYA_ERR_SHAPE, "block bounds: strides too small");
+  if (n == 0) return ALAYA_OK;
+  const int blocks = n_heads * ((n + 127) / 128);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == ALAYA_BF16)
+    block_bounds_kernel<__nv_bfloat16><<<blocks, 128, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(d_k), head_stride, n, dim, static_cast<__nv_bfloat16*>(d_bounds),
+        bounds_head_stride);
+  else if (dtype == ALAYA_F32)
+    block_bounds_kernel<float><<<blocks, 128, 0, st>>>(
+        static_cast<const float*>(d_k), head_stride, n, dim, static_cast<float*>(d_bounds), bounds_head_stride);
+  else
+    return fail(ALAYA_ERR_ARG, "bad dtype");
+  return cuda_check("block_bounds_kernel");
+}
+
+int* alaya_ws_block_stats(const alaya_params* p, const alaya_seq* seqs, int batch, void* d_ws) {
+  static thread_local Batch bt;
+  if (build_batch(p, seqs, batch, &bt) != ALAYA_OK) return nullptr;
+  const Layout L = layout_for(bt);
+  return reinterpret_cast<int*>(static_cast<char*>(d_ws) + L.counters) + 2;
+}
 
 int alaya_window_append(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_k,
                         const float* d_v, void* stream) {
@@ -263,6 +303,7 @@ int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch
   if (cudaMemsetAsync(c.ws.status, 0, 4, c.stream) != cudaSuccess) return cuda_check("memset");
   if (c.use_tc && fused_enabled()) {  // scan + attend in one persistent kernel
     if (cudaMemsetAsync(c.ws.gmax, 0, c.L.zero_bytes, c.stream) != cudaSuccess) return cuda_check("memset");
+    if (c.bt.block_filter && (rc = c.st.filter(c.bt, d_q, c.ws, c.stream))) return rc;
     if ((rc = launch_tc_fused(c.bt, c.seqs, d_q, c.ws, c.stream))) return rc;
     return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);
   }

@@ -31,6 +31,8 @@ struct KSeq {
   int32_t w;     // session-window rows
   int32_t chunk_base;  // first work chunk of this sequence
   int32_t nch;         // chunks per kv head
+  const void* bnd;     // block bounds [Hkv][bhs] ([block][2][D]) or null
+  int64_t bhs;
 };
 
 struct Batch {
@@ -41,6 +43,7 @@ struct Batch {
   int32_t total_chunks;
   float inv_sqrt_d;
   int32_t dbg;  // diagnostics only (ALAYA_TC_DBG): bit0 no L2 hint, bit1 no epilogue math, bit2 no MMA
+  int32_t block_filter;
 };
 
 // Workspace pointers (device), carved from the caller's buffer.
@@ -58,7 +61,8 @@ struct Ws {
   float* cscore;    // [chunks*G*chunk]
   float* partbuf;   // [B*Hq*(D+2)]
   float* smaxbuf;   // [B*Hq]
-  int* bfkeep;      // [chunks] block-filter flags (reserved)
+  unsigned long long* keep;  // [chunks] block-filter masks: bit t = 128-key tile t of the chunk kept
+  uint32_t* lbu;    // [B*Hq] encoded lower bound of the DIPR max (block filter); zeroed with gmax
 };
 
 __device__ __forceinline__ uint32_t enc_max(float f) {
@@ -82,6 +86,14 @@ __device__ __forceinline__ void decode_chunk(const Batch& bt, int c, int& b, int
   int local = c - bt.s[b].chunk_base;
   h = local / bt.s[b].nch;
   ci = local - h * bt.s[b].nch;
+}
+
+// Tiles (128 keys) of a chunk the scan must read: all of them, or the block
+// filter's mask.
+__device__ __forceinline__ unsigned long long chunk_tiles(const Batch& bt, const Ws& ws, int c,
+                                                          int ntiles) {
+  const unsigned long long all = ntiles >= 64 ? ~0ull : ((1ull << ntiles) - 1ull);
+  return bt.block_filter ? (ws.keep[c] & all) : all;
 }
 
 // Window membership of a GLOBAL base id (WindowConfig.base_ids, core.py:159-165).

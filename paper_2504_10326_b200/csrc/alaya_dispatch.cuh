@@ -40,6 +40,14 @@ struct Stages {
     attend_kernel<T, D, G><<<(unsigned)blocks, kThreads, 0, st>>>(bt, q, smax, ws, want_values);
     return cuda_check("attend_kernel");
   }
+  static int filter(const Batch& bt, const float* q, const Ws& ws, cudaStream_t st) {
+    if (bt.total_chunks == 0) return ALAYA_OK;
+    const int rows = bt.B * bt.Hq;
+    window_lb_kernel<T, D, G><<<(rows + kWarps - 1) / kWarps, kThreads, 0, st>>>(bt, q, ws);
+    block_filter_kernel<T, D, G><<<bt.total_chunks, kThreads, 0, st>>>(bt, q, ws, 0);  // LB
+    block_filter_kernel<T, D, G><<<bt.total_chunks, kThreads, 0, st>>>(bt, q, ws, 1);  // masks
+    return cuda_check("block filter");
+  }
   static int combine(const Batch& bt, const float* smax, const Ws& ws, float* out,
                      float* part_out, float* smax_out, cudaStream_t st) {
     const int rows = bt.B * bt.Hq;
@@ -50,6 +58,7 @@ struct Stages {
 
 using ScanFn = int (*)(const Batch&, const float*, const Ws&, cudaStream_t);
 using AttendFn = int (*)(const Batch&, const float*, const float*, const Ws&, int, cudaStream_t);
+using FilterFn = int (*)(const Batch&, const float*, const Ws&, cudaStream_t);
 using CombineFn = int (*)(const Batch&, const float*, const Ws&, float*, float*, float*,
                           cudaStream_t);
 
@@ -57,11 +66,13 @@ struct StageSet {
   ScanFn scan;
   AttendFn attend;
   CombineFn combine;
+  FilterFn filter;
 };
 
 template <typename T, int D, int G>
 StageSet make_set() {
-  return {&Stages<T, D, G>::scan, &Stages<T, D, G>::attend, &Stages<T, D, G>::combine};
+  return {&Stages<T, D, G>::scan, &Stages<T, D, G>::attend, &Stages<T, D, G>::combine,
+          &Stages<T, D, G>::filter};
 }
 
 template <typename T, int D>

@@ -46,8 +46,8 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
   uint8_t* a_ring = smem;
   uint8_t* b_buf = a_ring + kStages * kTileBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(b_buf + 2 * kBBytes);
-  // full[S], empty[S], accf[kAcc], acce[kAcc], cfull[Q], cempty[Q]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2 * kAcc + 2 * kQueue);
+  // full[S], empty[S], accf[kAcc], acce[kAcc], cfull[Q], cempty[Q], bfree[2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2 * kAcc + 2 * kQueue + 2);
   int* chunk_q = reinterpret_cast<int*>(tmem_slot + 4);              // [kQueue]
   int* s_t_all = chunk_q + kQueue;                                    // [kAttnWarps][2][32]
   float* s_w_all = reinterpret_cast<float*>(s_t_all + kAttnWarps * 64);
@@ -59,12 +59,14 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
   const uint32_t accf0 = bar0 + 8u * (2 * kStages), acce0 = accf0 + 8u * kAcc;
   auto cfull_bar = [&](int i) { return acce0 + 8u * (kAcc + i); };
   auto cempty_bar = [&](int i) { return acce0 + 8u * (kAcc + kQueue + i); };
+  const uint32_t bfree0 = acce0 + 8u * (kAcc + 2 * kQueue);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 1); }
     for (int a = 0; a < kAcc; ++a) { mbar_init(accf0 + 8u * a, 1); mbar_init(acce0 + 8u * a, 4); }
     // consumers of a queue slot: the MMA warp and the 4 epilogue warps
     for (int i = 0; i < kQueue; ++i) { mbar_init(cfull_bar(i), 1); mbar_init(cempty_bar(i), 5); }
+    for (int i = 0; i < 2; ++i) mbar_init(bfree0 + 8u * i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -99,8 +101,9 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
         const int valid = min(chunk, bt.s[b].n - ci * chunk);
         const int ntiles = (valid + kTileKeys - 1) / kTileKeys;
         const CUtensorMap* map = &maps.m[maps.map_of_seq[b]];
-        const int row0 = (int)(maps.row0_of_seq[b] + h * maps.rows_per_head[b] + (int64_t)ci * chunk);
-        for (int tl = 0; tl < ntiles; ++tl) {
+        const int row0 = (int)(h * maps.rows_per_head[b] + (int64_t)ci * chunk);
+        for (unsigned long long m = chunk_tiles(bt, ws, c, ntiles); m; m &= m - 1) {
+          const int tl = __ffsll((long long)m) - 1;
           mbar_wait(empty_bar(stage), phase ^ 1);
           mbar_expect_tx(full_bar(stage), kTileBytes);
           const uint32_t dst = smem_u32(a_ring + stage * kTileBytes);
@@ -113,8 +116,8 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     const uint32_t idesc = idesc_bf16<NP>();
-    int stage = 0, acc = 0, cidx = 0, slot = 0;
-    uint32_t phase = 0, ephase = 0, qphase = 0;
+    int stage = 0, acc = 0, cidx = 0, slot = 0, bcnt = 0;
+    uint32_t phase = 0, ephase = 0, qphase = 0, bphase = 0;
     for (;; ++cidx) {
       mbar_wait(cfull_bar(slot), qphase);
       const int c = chunk_q[slot];
@@ -126,12 +129,17 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
       decode_chunk(bt, c, b, h, ci);
       const int valid = min(chunk, bt.s[b].n - ci * chunk);
       const int ntiles = (valid + kTileKeys - 1) / kTileKeys;
-      uint8_t* bb = b_buf + (cidx & 1) * kBBytes;
-      for (int tl = 0; tl < ntiles; ++tl) {
+      const int bi = bcnt & 1;
+      uint8_t* bb = b_buf + bi * kBBytes;
+      bool first = true;
+      for (unsigned long long m = chunk_tiles(bt, ws, c, ntiles); m; m &= m - 1) {
         mbar_wait(acce0 + 8u * acc, ((ephase >> acc) & 1u) ^ 1u);
         ephase ^= 1u << acc;
         fence_after();
-        if (tl == 0) {
+        if (first) {
+          first = false;
+          mbar_wait(bfree0 + 8u * bi, ((bphase >> bi) & 1u) ^ 1u);  // last reader done
+          bphase ^= 1u << bi;
           build_b<G, NP>(bb, q + ((size_t)b * bt.Hq + (size_t)h * G) * 128, lane);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
@@ -146,6 +154,11 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
         acc = (acc + 1) % kAcc;
+      }
+      if (!first) {  // this chunk used B buffer bi: free it once its MMAs complete
+        if (lane == 0) mma_commit(bfree0 + 8u * bi);
+        __syncwarp();
+        ++bcnt;
       }
     }
   } else if (warp < kScanWarps) {
@@ -205,7 +218,7 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
 inline size_t fused_smem_bytes(int G, int kStages) {
   const int NP = (3 * G <= 16) ? 16 : 32;
   return 1024 + (size_t)kStages * tc::kTileBytes + 2 * 2 * NP * 128 +
-         8 * (2 * kStages + 2 * tc::kAcc + 2 * kQueue) + 16 + 4 * kQueue + kAttnWarps * 64 * 8 + 64;
+         8 * (2 * kStages + 2 * tc::kAcc + 2 * kQueue + 2) + 16 + 4 * kQueue + kAttnWarps * 64 * 8 + 64;
 }
 
 }  // namespace fused

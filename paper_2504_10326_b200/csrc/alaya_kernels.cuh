@@ -101,14 +101,25 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
     }
   };
 
-  if (ntiles > 0) load_tile(0, fa);
-  for (int tile = 0; tile < ntiles; tile += 2) {
-    if (tile + 1 < ntiles) load_tile(tile + 1, fb);
-    compute_tile(tile, fa);
-    if (tile + 1 < ntiles) {
-      if (tile + 2 < ntiles) load_tile(tile + 2, fa);
-      compute_tile(tile + 1, fb);
-    }
+  // kept tiles (block filter), double-buffered: load the next while computing
+  const unsigned long long tmask = chunk_tiles(bt, ws, blockIdx.x, ntiles);
+  unsigned long long mrem = tmask;
+  auto pop = [&]() -> int {
+    if (!mrem) return -1;
+    const int t = __ffsll((long long)mrem) - 1;
+    mrem &= mrem - 1;
+    return t;
+  };
+  int cur = pop();
+  if (cur >= 0) load_tile(cur, fa);
+  while (cur >= 0) {
+    const int nxt = pop();
+    if (nxt >= 0) load_tile(nxt, fb);
+    compute_tile(cur, fa);
+    if (nxt < 0) break;
+    cur = pop();
+    if (cur >= 0) load_tile(cur, fa);
+    compute_tile(nxt, fb);
   }
 
   // chunk max per head, then the global running max (order-preserving atomic)
@@ -138,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
     int cnt = 0;
     for (int r = 0; r < seg; r += 32) {
       int pos = sbeg + r + lane;
-      bool p = pos < valid && sc[j * chunk + pos] >= th;
+      bool p = pos < valid && ((tmask >> (pos / kScanTile)) & 1ull) && sc[j * chunk + pos] >= th;
       cnt += __popc(__ballot_sync(kFull, p));
     }
     cntj[j] = cnt;
@@ -161,8 +172,9 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
     if (cntj[j] > 0) {
       for (int r = 0; r < seg; r += 32) {
         int pos = sbeg + r + lane;
-        float v = pos < valid ? sc[j * chunk + pos] : -INFINITY;
-        bool p = pos < valid && v >= th;
+        const bool live = pos < valid && ((tmask >> (pos / kScanTile)) & 1ull);
+        float v = live ? sc[j * chunk + pos] : -INFINITY;
+        bool p = live && v >= th;
         unsigned bal = __ballot_sync(kFull, p);
         if (p) {
           int o = off + __popc(bal & lanemask_lt());
@@ -524,6 +536,231 @@ __global__ void __launch_bounds__(kThreads)
       if (e == 0) { pr[0] = empty ? -INFINITY : m; pr[1] = empty ? 0.f : l; }
       pr[2 + e] = empty ? 0.f : a;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Coarse block filter. Per 128-token block the index holds (K dtype):
+//   row 0 lo[d], row 1 hi[d]      per-dim box
+//   row 2 mu[d]                   block mean (as stored)
+//   row 3 rep[d]                  largest-L2-norm key (index.py:217-228, r=1)
+//   row 4 [0] = radius            max_k ||k - mu||, rounded up
+// Per call: LB_j = max(score of the base-window keys, score of every block's
+// representative) minus a rounding margin -- real scores, hence a lower bound
+// of the DIPR max; a 128-key tile is read only if some head of the group has
+// min(box, ball) upper bound + margin >= LB_j - beta. Exact by construction.
+// ---------------------------------------------------------------------------
+constexpr int kBndRows = 5;
+
+template <typename T>
+__device__ __forceinline__ float to_f(T x) {
+  if constexpr (std::is_same_v<T, float>) return x; else return __bfloat162float(x);
+}
+
+template <typename T, int D, int G>
+__global__ void __launch_bounds__(kThreads) window_lb_kernel(const __grid_constant__ Batch bt,
+                                                             const float* __restrict__ q, Ws ws) {
+  constexpr int DL = (D + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (row >= bt.B * bt.Hq) return;
+  const int b = row / bt.Hq, qh = row - b * bt.Hq, h = qh / G;
+  const KSeq& s = bt.s[b];
+  const int64_t P = s.P, off = s.off;
+  int64_t a0 = 0, a1, b0, b1;
+  if (P <= (int64_t)bt.wi + bt.wl) { a1 = P; b0 = 0; b1 = 0; }
+  else { a1 = bt.wi; b0 = P - bt.wl; b1 = P; }
+  a0 = max(a0, off) - off; a1 = min(a1, off + s.n) - off; if (a1 < a0) a1 = a0;
+  b0 = max(b0, off) - off; b1 = min(b1, off + s.n) - off; if (b1 < b0) b1 = b0;
+  const int na = (int)(a1 - a0), R = na + (int)(b1 - b0);
+  float qr[DL];
+#pragma unroll
+  for (int k = 0; k < DL; ++k) qr[k] = lane + 32 * k < D ? q[(size_t)row * D + lane + 32 * k] : 0.f;
+  const T* kb = reinterpret_cast<const T*>(s.k) + (size_t)h * s.hs;
+  float lb = -INFINITY;
+  for (int r = 0; r < R; ++r) {
+    const T* kr = kb + (size_t)(r < na ? a0 + r : b0 + r - na) * D;
+    float a = 0.f, mag = 0.f;
+#pragma unroll
+    for (int k = 0; k < DL; ++k) {
+      const int e = lane + 32 * k;
+      if (e < D) {
+        const float x = to_f(kr[e]);
+        a = fmaf(qr[k], x, a);
+        mag = fmaf(fabsf(qr[k]), fabsf(x), mag);
+      }
+    }
+    a = warp_sum(a);
+    mag = warp_sum(mag);
+    lb = fmaxf(lb, a - 1e-3f * (mag + 1.f));  // margin covers any scan/score rounding
+  }
+  if (lane == 0 && lb > -INFINITY) atomicMax(&ws.lbu[row], enc_max(lb));
+}
+
+// Per chunk: representative-key lower bound (pass 0) or keep mask (pass 1).
+template <typename T, int D, int G>
+__global__ void __launch_bounds__(kThreads) block_filter_kernel(const __grid_constant__ Batch bt,
+                                                                const float* __restrict__ q, Ws ws,
+                                                                int pass) {
+  constexpr int DL = (D + 31) / 32;
+  __shared__ unsigned long long s_mask;
+  __shared__ int s_kept;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.x;
+  int b, h, ci;
+  decode_chunk(bt, c, b, h, ci);
+  const KSeq& s = bt.s[b];
+  const int chunk = bt.chunk;
+  const int valid = min(chunk, s.n - ci * chunk);
+  const int ntiles = (valid + 127) / 128;
+  if (threadIdx.x == 0) { s_mask = 0ull; s_kept = 0; }
+  float qr[G][DL], qn[G], thr[G];
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    const size_t row = (size_t)b * bt.Hq + h * G + j;
+    float n2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < DL; ++k) {
+      qr[j][k] = lane + 32 * k < D ? q[row * D + lane + 32 * k] : 0.f;
+      n2 = fmaf(qr[j][k], qr[j][k], n2);
+    }
+    qn[j] = sqrtf(warp_sum(n2)) * (1.f + 1e-6f);
+    thr[j] = pass ? dec_max(ws.lbu[row]) - bt.beta : 0.f;
+  }
+  __syncthreads();
+  const T* bb = reinterpret_cast<const T*>(s.bnd) + (size_t)h * s.bhs;
+  float lbj[G];
+#pragma unroll
+  for (int j = 0; j < G; ++j) lbj[j] = -INFINITY;
+  for (int t = warp; t < ntiles; t += kWarps) {
+    const int blk = (ci * chunk) / 128 + t;
+    const T* lo = bb + (size_t)blk * kBndRows * D;
+    const T* hi = lo + D;
+    const T* mu = lo + 2 * D;
+    const T* rep = lo + 3 * D;
+    const float rad = to_f(lo[4 * D]);
+    bool keep = false;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      if (pass == 0) {  // representative score: a real key's score
+        float a = 0.f, mag = 0.f;
+#pragma unroll
+        for (int k = 0; k < DL; ++k) {
+          const int e = lane + 32 * k;
+          if (e < D) {
+            const float x = to_f(rep[e]);
+            a = fmaf(qr[j][k], x, a);
+            mag = fmaf(fabsf(qr[j][k]), fabsf(x), mag);
+          }
+        }
+        a = warp_sum(a);
+        mag = warp_sum(mag);
+        lbj[j] = fmaxf(lbj[j], a - 1e-3f * (mag + 1.f));
+      } else {
+        float ubox = 0.f, qm = 0.f, mag = 0.f;
+#pragma unroll
+        for (int k = 0; k < DL; ++k) {
+          const int e = lane + 32 * k;
+          if (e < D) {
+            const float m = fmaxf(qr[j][k] * to_f(lo[e]), qr[j][k] * to_f(hi[e]));
+            ubox += m;
+            const float pm = qr[j][k] * to_f(mu[e]);
+            qm += pm;
+            mag += fabsf(m) + fabsf(pm);
+          }
+        }
+        ubox = warp_sum(ubox);
+        qm = warp_sum(qm);
+        mag = warp_sum(mag);
+        const float ub = fminf(ubox, qm + qn[j] * rad);
+        keep |= ub + 1e-3f * (mag + qn[j] * rad + 1.f) >= thr[j];  // thr = -inf keeps all
+      }
+    }
+    if (pass == 1 && lane == 0 && keep) {
+      atomicOr(&s_mask, 1ull << t);
+      atomicAdd(&s_kept, 1);
+    }
+  }
+  if (pass == 0) {
+    if (lane < G) {
+#pragma unroll
+      for (int j = 0; j < G; ++j)
+        if (j == lane && lbj[j] > -INFINITY) atomicMax(&ws.lbu[(size_t)b * bt.Hq + h * G + j], enc_max(lbj[j]));
+    }
+    return;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ws.keep[c] = s_mask;
+    atomicAdd(&ws.counters[2], s_kept);
+    atomicAdd(&ws.counters[3], ntiles);
+  }
+}
+
+// Build the block index of a slab: one CTA of 128 threads per (head, block).
+template <typename T>
+__global__ void __launch_bounds__(128) block_bounds_kernel(const T* __restrict__ k, int64_t hs, int n,
+                                                           int D, T* __restrict__ bounds, int64_t bhs) {
+  __shared__ float mu_s[256];
+  __shared__ float wbest[4], wrad[4];
+  __shared__ int wrow[4];
+  const int nblk = (n + 127) / 128;
+  const int h = blockIdx.x / nblk, blk = blockIdx.x - h * nblk;
+  const int r0 = blk * 128, r1 = min(n, r0 + 128);
+  const T* kh = k + (size_t)h * hs;
+  T* out = bounds + (size_t)h * bhs + (size_t)blk * kBndRows * D;
+  for (int e = threadIdx.x; e < D; e += blockDim.x) {
+    float lo = INFINITY, hi = -INFINITY, sum = 0.f;
+    for (int r = r0; r < r1; ++r) {
+      const float x = to_f(kh[(size_t)r * D + e]);
+      lo = fminf(lo, x);
+      hi = fmaxf(hi, x);
+      sum += x;
+    }
+    T mu;
+    if constexpr (std::is_same_v<T, float>) { out[e] = lo; out[D + e] = hi; mu = sum / (r1 - r0); }
+    else {
+      out[e] = __float2bfloat16_rn(lo);  // exact: the inputs are bf16
+      out[D + e] = __float2bfloat16_rn(hi);
+      mu = __float2bfloat16_rn(sum / (r1 - r0));
+    }
+    out[2 * D + e] = mu;
+    mu_s[e] = to_f(mu);
+  }
+  __syncthreads();
+  // per row: squared norm (representative) and squared distance to mu (radius)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float best = -1.f, rad2 = 0.f;
+  int brow = r0;
+  for (int r = r0 + warp; r < r1; r += 4) {
+    float nn = 0.f, dd = 0.f;
+    for (int e = lane; e < D; e += 32) {
+      const float x = to_f(kh[(size_t)r * D + e]);
+      nn = fmaf(x, x, nn);
+      dd = fmaf(x - mu_s[e], x - mu_s[e], dd);
+    }
+    nn = warp_sum(nn);
+    dd = warp_sum(dd);
+    if (nn > best) { best = nn; brow = r; }  // rows ascend per warp: ties keep the first
+    rad2 = fmaxf(rad2, dd);
+  }
+  if (lane == 0) { wbest[warp] = best; wrow[warp] = brow; wrad[warp] = rad2; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float bb = -1.f, rr = 0.f;
+    int br = r0;
+    for (int w = 0; w < 4; ++w) {
+      if (wbest[w] > bb || (wbest[w] == bb && wrow[w] < br)) { bb = wbest[w]; br = wrow[w]; }
+      rr = fmaxf(rr, wrad[w]);
+    }
+    wrow[0] = br;
+    wrad[0] = sqrtf(rr) * (1.f + 1e-5f) + 1e-6f;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < D; e += blockDim.x) {
+    out[3 * D + e] = kh[(size_t)wrow[0] * D + e];
+    if constexpr (std::is_same_v<T, float>) out[4 * D + e] = e == 0 ? wrad[0] : 0.f;
+    else out[4 * D + e] = e == 0 ? __float2bfloat16_ru(wrad[0]) : __float2bfloat16_rn(0.f);  // round up: sound
   }
 }
 

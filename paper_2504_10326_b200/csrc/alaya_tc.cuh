@@ -33,7 +33,6 @@ constexpr int kMaxMaps = 128;
 struct Maps {
   CUtensorMap m[kMaxMaps];
   int16_t map_of_seq[ALAYA_MAX_BATCH];
-  int64_t row0_of_seq[ALAYA_MAX_BATCH];  // tensor-map row of (seq, head 0, token 0)
   int64_t rows_per_head[ALAYA_MAX_BATCH];
 };
 
@@ -162,7 +161,8 @@ __device__ __forceinline__ void epilogue_chunk(const Batch& bt, const Ws& ws, in
   }
   const size_t cbase = (size_t)c * G;
   const int qoff = quarter * (chunk / 4);
-  for (int tl = 0; tl < ntiles; ++tl) {
+  for (unsigned long long m = chunk_tiles(bt, ws, c, ntiles); m; m &= m - 1) {
+    const int tl = __ffsll((long long)m) - 1;
     mbar_wait(accf0 + 8u * acc, (aphase >> acc) & 1u);
     fence_after();
     float v[NP];
@@ -222,18 +222,20 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 3 : (kStages <= 3 
   uint8_t* a_ring = smem;                                     // kStages x 32 KB
   uint8_t* b_buf = a_ring + kStages * kTileBytes;             // 2 x kBBytes
   uint64_t* bars = reinterpret_cast<uint64_t*>(b_buf + 2 * kBBytes);
-  // full[kStages], empty[kStages], accf[kAcc], acce[kAcc]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2 * kAcc);
+  // full[kStages], empty[kStages], accf[kAcc], acce[kAcc], bfree[2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2 * kAcc + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar0 = smem_u32(bars);
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (kStages + s); };
   const uint32_t accf0 = bar0 + 8u * (2 * kStages), acce0 = accf0 + 8u * kAcc;
+  const uint32_t bfree0 = acce0 + 8u * kAcc;  // B buffer free: MMAs reading it completed
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 1); }
     for (int a = 0; a < kAcc; ++a) { mbar_init(accf0 + 8u * a, 1); mbar_init(acce0 + 8u * a, 4); }
+    for (int i = 0; i < 2; ++i) mbar_init(bfree0 + 8u * i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -261,8 +263,9 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 3 : (kStages <= 3 
         const int valid = min(chunk, bt.s[b].n - ci * chunk);
         const int ntiles = (valid + kTileKeys - 1) / kTileKeys;
         const CUtensorMap* map = &maps.m[maps.map_of_seq[b]];
-        const int row0 = (int)(maps.row0_of_seq[b] + h * maps.rows_per_head[b] + (int64_t)ci * chunk);
-        for (int tl = 0; tl < ntiles; ++tl) {
+        const int row0 = (int)(h * maps.rows_per_head[b] + (int64_t)ci * chunk);
+        for (unsigned long long m = chunk_tiles(bt, ws, c, ntiles); m; m &= m - 1) {
+          const int tl = __ffsll((long long)m) - 1;
           mbar_wait(empty_bar(stage), phase ^ 1);
           mbar_expect_tx(full_bar(stage), kTileBytes);
           const uint32_t dst = smem_u32(a_ring + stage * kTileBytes);
@@ -280,21 +283,25 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 3 : (kStages <= 3 
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     const uint32_t idesc = idesc_bf16<NP>();
-    int stage = 0, acc = 0, cidx = 0;
-    uint32_t phase = 0, ephase = 0;
+    int stage = 0, acc = 0, cidx = 0, bcnt = 0;
+    uint32_t phase = 0, ephase = 0, bphase = 0;
     for (int c = blockIdx.x; c < bt.total_chunks; c += gridDim.x, ++cidx) {
       int b, h, ci;
       decode_chunk(bt, c, b, h, ci);
       const int valid = min(chunk, bt.s[b].n - ci * chunk);
       const int ntiles = (valid + kTileKeys - 1) / kTileKeys;
-      uint8_t* bb = b_buf + (cidx & 1) * kBBytes;
-      for (int tl = 0; tl < ntiles; ++tl) {
+      const int bi = bcnt & 1;
+      uint8_t* bb = b_buf + bi * kBBytes;
+      bool first = true;
+      for (unsigned long long m = chunk_tiles(bt, ws, c, ntiles); m; m &= m - 1) {
         mbar_wait(acce0 + 8u * acc, ((ephase >> acc) & 1u) ^ 1u);
         ephase ^= 1u << acc;
         fence_after();
-        if (tl == 0) {
-          // the MMAs that last read this B buffer (previous chunk of this
-          // parity) are complete: the acc_empty wait covers kAcc tiles back.
+        if (first) {
+          first = false;
+          // wait until the MMAs that last read this B buffer have completed
+          mbar_wait(bfree0 + 8u * bi, ((bphase >> bi) & 1u) ^ 1u);
+          bphase ^= 1u << bi;
           build_b<G, NP>(bb, q + ((size_t)b * bt.Hq + (size_t)h * G) * 128, lane);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
@@ -310,6 +317,11 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 3 : (kStages <= 3 
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
         acc = (acc + 1) % kAcc;
+      }
+      if (!first) {  // this chunk used B buffer bi: free it once its MMAs complete
+        if (lane == 0) mma_commit(bfree0 + 8u * bi);
+        __syncwarp();
+        ++bcnt;
       }
     }
   } else {
@@ -332,7 +344,7 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 3 : (kStages <= 3 
 
 inline size_t tc_smem_bytes(int G, int kStages) {
   const int NP = (3 * G <= 16) ? 16 : 32;
-  return 1024 + (size_t)kStages * kTileBytes + 2 * 2 * NP * 128 + 8 * (2 * kStages + 2 * kAcc) + 64;
+  return 1024 + (size_t)kStages * kTileBytes + 2 * 2 * NP * 128 + 8 * (2 * kStages + 2 * kAcc + 2) + 64;
 }
 
 }  // namespace tc

@@ -80,7 +80,6 @@ int build_maps(const Batch& bt, const alaya_seq* seqs, tc::Maps& maps) {
   int nmaps = 0;
   for (int b = 0; b < bt.B; ++b) {
     maps.map_of_seq[b] = 0;
-    maps.row0_of_seq[b] = 0;
     maps.rows_per_head[b] = seqs[b].head_stride / 128;
     if (seqs[b].n == 0) continue;
     int found = -1;

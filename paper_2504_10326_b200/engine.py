@@ -52,6 +52,7 @@ class SeqView:
     w: int = 0
     token_offset: int = 0
     prefix_len: int | None = None
+    bounds: torch.Tensor | None = None  # [Hkv, blocks, 5, d] (block_bounds), block filter only
 
 
 def _check_kv(t: torch.Tensor, name: str, dtype, d: int) -> None:
@@ -95,6 +96,10 @@ def seq_array(seqs: list[SeqView], params: AlayaParams, dtype: torch.dtype):
             if s.wk.shape[1] < s.w or s.wv.stride(0) != s.wk.stride(0):
                 raise ValueError("window K/V shape mismatch")
             e.wk, e.wv, e.w_head_stride = s.wk.data_ptr(), s.wv.data_ptr(), s.wk.stride(0)
+        if s.bounds is not None:
+            if s.bounds.dtype != dtype or not s.bounds.is_contiguous() or s.bounds.shape[0] != params.n_kv_heads:
+                raise ValueError("bounds must be a contiguous [Hkv, blocks, 5, d] tensor in the KV dtype")
+            e.bounds, e.bounds_head_stride = s.bounds.data_ptr(), s.bounds.stride(0)
         e.n, e.w = int(s.n), int(s.w)
         e.token_offset = int(s.token_offset)
         e.prefix_len = int(s.n + s.token_offset if s.prefix_len is None else s.prefix_len)
@@ -166,6 +171,14 @@ class Call:
         """Stage 1 alone (no max export): used to time the scan kernel."""
         check(self.lib.alaya_scan(ctypes.byref(self.params), self.seqs, self.B, q.data_ptr(),
                                   None, self.ws.data_ptr(), self.ws_bytes, self.stream))
+
+    def block_stats(self) -> tuple[int, int]:
+        """(128-key blocks kept, blocks considered) by the block filter in the last scan."""
+        p = self.lib.alaya_ws_block_stats(ctypes.byref(self.params), self.seqs, self.B,
+                                          self.ws.data_ptr())
+        off = p - self.ws.data_ptr()
+        v = self.ws[off:off + 8].view(torch.int32).tolist()
+        return int(v[0]), int(v[1])
 
     def status(self) -> int:
         """Device status word of the last dipr_attention (synchronises)."""
@@ -256,3 +269,22 @@ def window_append(seqs: list[SeqView], params: AlayaParams, dtype: torch.dtype,
     v = v.to(torch.float32).contiguous()
     check(lib.alaya_window_append(ctypes.byref(params), arr, len(seqs), k.data_ptr(), v.data_ptr(),
                                   torch.cuda.current_stream(k.device).cuda_stream))
+
+
+def block_bounds(k: torch.Tensor) -> torch.Tensor:
+    """Coarse block index of a ``[Hkv, n, d]`` key slab -> ``[Hkv, ceil(n/128), 5, d]``
+    in the key dtype: per 128-token block the per-dim min and max, the mean, the
+    largest-norm key (reference representative, ``index.py:217-228``) and the
+    radius ``max ||k - mean||`` (row 4, element 0, rounded up)."""
+    require_cuda()
+    lib = _lib.load()
+    if k.dtype not in _DTYPES:
+        raise ValueError(f"unsupported KV dtype {k.dtype}")
+    if k.dim() != 3 or k.stride(2) != 1 or k.stride(1) != k.shape[2]:
+        raise ValueError("keys must be [heads, rows, d] with unit row stride")
+    hkv, n, d = k.shape
+    out = torch.empty(hkv, (n + 127) // 128, 5, d, dtype=k.dtype, device=k.device)
+    check(lib.alaya_block_bounds(k.data_ptr(), _DTYPES[k.dtype], hkv, k.stride(0), n, d,
+                                 out.data_ptr(), out.stride(0),
+                                 torch.cuda.current_stream(k.device).cuda_stream))
+    return out

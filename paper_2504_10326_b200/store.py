@@ -61,6 +61,7 @@ class ContextRecord:
     shape: ModelShape
     plans: dict[int, Plan]
     indexes: dict = field(default_factory=dict)
+    bounds: torch.Tensor | None = None  # [L, Hkv, blocks, 2, d] coarse block index (block filter)
 
     @property
     def length(self) -> int:
@@ -294,9 +295,12 @@ class Session:
     def _seq_view(self, layer: int) -> engine.SeqView:
         p = self.reused_prefix_len if self.base is not None else 0
         w = self._wlen[layer]
+        bnd = None
+        if p and self._store.config.block_filter:
+            bnd = self._store._bounds_for(self.base)[layer]
         return engine.SeqView(
             k=self.base.keys[layer] if p else None, v=self.base.values[layer] if p else None, n=p,
-            wk=self._wk[layer] if w else None, wv=self._wv[layer] if w else None, w=w)
+            wk=self._wk[layer] if w else None, wv=self._wv[layer] if w else None, w=w, bounds=bnd)
 
     def _exec_params(self, active: Plan):
         """(beta, window initial, window last) the kernels run for a plan."""
@@ -382,6 +386,14 @@ class ContextStore:
     def get(self, context_id: str) -> ContextRecord:
         return self.contexts[context_id]
 
+    def _bounds_for(self, record: ContextRecord) -> torch.Tensor:
+        """Coarse block index of a context, built on first use (``index.py:231-243``
+        builds the reference's BlockIndex at import; this one holds sound boxes)."""
+        if record.bounds is None:
+            record.bounds = torch.stack([engine.block_bounds(record.keys[l])
+                                         for l in range(self.shape.n_layers)])
+        return record.bounds
+
     def _append_params(self):
         sh = self.shape
         return engine.make_params(sh.n_query_heads, sh.n_kv_heads, sh.dim, self.kv_dtype, 0.0, 0, 0)
@@ -391,7 +403,8 @@ class ContextStore:
         only the window row counts change between decode steps."""
         views = [s._seq_view(layer) for s in sessions]
         sig = tuple((v.k.data_ptr() if v.k is not None else 0, v.n,
-                     v.wk.data_ptr() if v.wk is not None else 0) for v in views)
+                     v.wk.data_ptr() if v.wk is not None else 0,
+                     v.bounds.data_ptr() if v.bounds is not None else 0) for v in views)
         key = (layer, tuple(id(s) for s in sessions), beta, wi, wl)
         hit = self._calls.get(key)
         if hit is not None and hit[0] == sig:

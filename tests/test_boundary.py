@@ -32,9 +32,9 @@ def test_struct_layout_matches_header(tmp_path):
 #include <stddef.h>
 #include "{HEADER}"
 int main(void) {{
-  printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(alaya_seq), offsetof(alaya_seq, n),
-         offsetof(alaya_seq, prefix_len), sizeof(alaya_params), offsetof(alaya_params, beta),
-         offsetof(alaya_params, block_filter));
+  printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(alaya_seq), offsetof(alaya_seq, n),
+         offsetof(alaya_seq, prefix_len), offsetof(alaya_seq, bounds), sizeof(alaya_params),
+         offsetof(alaya_params, beta), offsetof(alaya_params, block_filter));
   return 0;
 }}''')
     exe = tmp_path / "layout"
@@ -42,8 +42,8 @@ int main(void) {{
     got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
                                           check=True).stdout.split()]
     S, P = _lib.AlayaSeq, _lib.AlayaParams
-    assert got == [ctypes.sizeof(S), S.n.offset, S.prefix_len.offset, ctypes.sizeof(P),
-                   P.beta.offset, P.block_filter.offset]
+    assert got == [ctypes.sizeof(S), S.n.offset, S.prefix_len.offset, S.bounds.offset,
+                   ctypes.sizeof(P), P.beta.offset, P.block_filter.offset]
 
 
 def _params(**kw):
