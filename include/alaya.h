@@ -171,6 +171,10 @@ int alaya_block_bounds(const void* d_k, int dtype, int n_heads, int64_t head_str
  * this workspace: device pointer to two int32 (valid after the scan). */
 int* alaya_ws_block_stats(const alaya_params* p, const alaya_seq* seqs, int batch, void* d_ws);
 
+/* Diagnostics: candidate-superset sizes of the last scan on this workspace,
+ * device pointer to int32 [total_chunks][G][4 scan sub-lists]. */
+int* alaya_ws_candidate_counts(const alaya_params* p, const alaya_seq* seqs, int batch, void* d_ws);
+
 /* Device status word of the last alaya_dipr_attention on this workspace
  * (ALAYA_OK or ALAYA_ERR_NONFINITE); pointer into d_ws. */
 int* alaya_ws_status(void* d_ws);

@@ -36,6 +36,7 @@ EXPORTS = (
     "alaya_last_error", "alaya_version", "alaya_workspace_bytes", "alaya_dipr_attention",
     "alaya_scan", "alaya_attend", "alaya_merge_partials", "alaya_merge_states", "alaya_selected",
     "alaya_ws_status", "alaya_window_append", "alaya_block_bounds", "alaya_ws_block_stats",
+    "alaya_ws_candidate_counts",
 )
 
 
@@ -104,6 +105,8 @@ def load() -> ctypes.CDLL:
     lib.alaya_window_append.argtypes = [P, S, i32, vp, vp, vp]
     lib.alaya_block_bounds.restype = i32
     lib.alaya_block_bounds.argtypes = [vp, i32, i32, ctypes.c_int64, i32, i32, vp, ctypes.c_int64, vp]
+    lib.alaya_ws_candidate_counts.restype = vp
+    lib.alaya_ws_candidate_counts.argtypes = [P, S, i32, vp]
     lib.alaya_ws_block_stats.restype = vp
     lib.alaya_ws_block_stats.argtypes = [P, S, i32, vp]
     lib.alaya_ws_status.restype = vp

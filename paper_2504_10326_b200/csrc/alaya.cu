@@ -1,6 +1,7 @@
 // C-ABI entry points (include/alaya.h): validation, workspace layout, kernel
 // dispatch over (dtype, dim, group size) and launch.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -105,6 +106,10 @@ int build_batch(const alaya_params* p, const alaya_seq* seqs, int B, Batch* bt) 
   bt->wl = p->win_last;
   bt->inv_sqrt_d = (float)(1.0 / std::sqrt((double)p->dim));
   bt->block_filter = p->block_filter ? 1 : 0;
+  {  // attend task split threshold; ALAYA_SPLIT overrides (diagnostics)
+    const char* e = getenv("ALAYA_SPLIT");
+    bt->split = (e && *e) ? atoi(e) : std::max(256, chunk / 4);
+  }
   int cb = 0;
   for (int b = 0; b < B; ++b) {
     const alaya_seq& s = seqs[b];
@@ -128,7 +133,7 @@ size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 struct Layout {
   size_t zero_bytes;
   size_t status, gmax, counters, cnt, selcnt, retcnt, part_l, part_acc, cidx, cscore, partbuf, smaxbuf,
-      keep, lbu, total;
+      keep, lbu, ovl_l, ovl_acc, ovl_sel, ovl_ret, heavy, ovlist, total;
 };
 
 Layout layout_for(const Batch& bt) {
@@ -145,6 +150,12 @@ Layout layout_for(const Batch& bt) {
   L.retcnt = o; o = align_up(o + 4 * C * G);
   L.part_l = o; o = align_up(o + 4 * C * G);
   L.part_acc = o; o = align_up(o + 4 * C * G * D);
+  L.ovl_l = o; o = align_up(o + 4 * C * G * 4);
+  L.ovl_acc = o; o = align_up(o + 4 * C * G * 4 * D);
+  L.ovl_sel = o; o = align_up(o + 4 * C * G * 4);
+  L.ovl_ret = o; o = align_up(o + 4 * C * G * 4);
+  L.heavy = o; o = align_up(o + 4 * C * G);
+  L.ovlist = o; o = align_up(o + 4 * C * G * 3);
   L.cidx = o; o = align_up(o + 4 * C * G * bt.chunk);
   L.cscore = o; o = align_up(o + 4 * C * G * bt.chunk);
   L.partbuf = o; o = align_up(o + 4 * rows * (D + 2));
@@ -171,6 +182,12 @@ Ws carve(const Layout& L, void* base) {
   w.partbuf = reinterpret_cast<float*>(c + L.partbuf);
   w.smaxbuf = reinterpret_cast<float*>(c + L.smaxbuf);
   w.keep = reinterpret_cast<unsigned long long*>(c + L.keep);
+  w.ovl_l = reinterpret_cast<float*>(c + L.ovl_l);
+  w.ovl_acc = reinterpret_cast<float*>(c + L.ovl_acc);
+  w.ovl_sel = reinterpret_cast<int*>(c + L.ovl_sel);
+  w.ovl_ret = reinterpret_cast<int*>(c + L.ovl_ret);
+  w.heavy = reinterpret_cast<int*>(c + L.heavy);
+  w.ovlist = reinterpret_cast<int*>(c + L.ovlist);
   w.lbu = reinterpret_cast<uint32_t*>(c + L.lbu);
   return w;
 }
@@ -266,6 +283,12 @@ int alaya_block_bounds(const void* d_k, int dtype, int n_heads, int64_t head_str
   return cuda_check("block_bounds_kernel");
 }
 
+int* alaya_ws_candidate_counts(const alaya_params* p, const alaya_seq* seqs, int batch, void* d_ws) {
+  static thread_local Batch bt;
+  if (build_batch(p, seqs, batch, &bt) != ALAYA_OK) return nullptr;
+  return reinterpret_cast<int*>(static_cast<char*>(d_ws) + layout_for(bt).cnt);
+}
+
 int* alaya_ws_block_stats(const alaya_params* p, const alaya_seq* seqs, int batch, void* d_ws) {
   static thread_local Batch bt;
   if (build_batch(p, seqs, batch, &bt) != ALAYA_OK) return nullptr;
@@ -304,6 +327,7 @@ int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch
   if (c.use_tc && fused_enabled()) {  // scan + attend in one persistent kernel
     if (cudaMemsetAsync(c.ws.gmax, 0, c.L.zero_bytes, c.stream) != cudaSuccess) return cuda_check("memset");
     if (c.bt.block_filter && (rc = c.st.filter(c.bt, d_q, c.ws, c.stream))) return rc;
+    c.bt.split = 0x7fffffff;  // the fused kernel runs whole (chunk, head) pairs
     if ((rc = launch_tc_fused(c.bt, c.seqs, d_q, c.ws, c.stream))) return rc;
     return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);
   }

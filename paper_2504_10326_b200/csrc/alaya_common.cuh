@@ -44,6 +44,7 @@ struct Batch {
   float inv_sqrt_d;
   int32_t dbg;  // diagnostics only (ALAYA_TC_DBG): bit0 no L2 hint, bit1 no epilogue math, bit2 no MMA
   int32_t block_filter;
+  int32_t split;  // attend task split threshold (candidates per (chunk, head) pair)
 };
 
 // Workspace pointers (device), carved from the caller's buffer.
@@ -51,12 +52,19 @@ struct Ws {
   int* status;
   uint32_t* gmax;   // [B*Hq] order-preserving encoded running max
   int* counters;    // [16] right after gmax (zeroed with it): [0] attend ticket, [1] scan ticket
+                    // (fused), [2..3] block-filter kept/total, [7] overflow items
   int* group_done;  // [B*Hkv] right after counters (zeroed with it): chunks published per group
   int* cnt;         // [chunks*G*4] candidate counts per scan sub-list (see CandList)
   int* selcnt;      // [chunks*G]
   int* retcnt;      // [chunks*G]
-  float* part_l;    // [chunks*G]
+  float* part_l;    // [chunks*G] primary (chunk, head) partials
   float* part_acc;  // [chunks*G*D]
+  float* ovl_l;     // [chunks*G*4] overflow sub-list partials (split pairs, q = 1..3)
+  float* ovl_acc;   // [chunks*G*4*D]
+  int* ovl_sel;     // [chunks*G*4]
+  int* ovl_ret;     // [chunks*G*4]
+  int* heavy;       // [chunks*G] 1 = pair split into sub-list tasks (written by the scan)
+  int* ovlist;      // [chunks*G*3] overflow items pair*4 + q (q = 1..3), count in counters[7]
   int* cidx;        // [chunks*G*chunk] candidate local row (then selected, compacted)
   float* cscore;    // [chunks*G*chunk]
   float* partbuf;   // [B*Hq*(D+2)]
@@ -118,6 +126,38 @@ struct CandList {
     return 3 * qcap + i - pre[3];
   }
 };
+// Virtual list over sub-lists [qb, qe) of one (chunk, head); phys() is relative
+// to sub-list qb's region.
+__device__ __forceinline__ CandList cand_range(const int* cnt4, int qb, int qe, int chunk,
+                                               bool through_l2) {
+  CandList L;
+  L.qcap = chunk / 4;
+  L.pre[0] = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int q = qb + k;
+    const int n = q < qe ? (through_l2 ? __ldcg(cnt4 + q) : cnt4[q]) : 0;
+    L.pre[k + 1] = L.pre[k] + n;
+  }
+  return L;
+}
+// Attend task split, decided by the scan at chunk end: a (chunk, head) pair with
+// more than bt.split candidates is processed as 4 sub-list tasks (sub-list 0 by
+// the primary task into the primary slot, sub-lists 1..3 into overflow slots).
+__device__ __forceinline__ void publish_pair(const Batch& bt, const Ws& ws, size_t cj, int total) {
+  const int hv = total > bt.split;
+  ws.heavy[cj] = hv;
+  if (hv) {
+    const int o = atomicAdd(&ws.counters[7], 3);
+    for (int k = 0; k < 3; ++k) ws.ovlist[o + k] = (int)cj * 4 + 1 + k;
+  }
+}
+__device__ __forceinline__ int pair_total(const int* cnt4, bool through_l2) {
+  const int4 v = through_l2 ? __ldcg(reinterpret_cast<const int4*>(cnt4))
+                            : *reinterpret_cast<const int4*>(cnt4);
+  return v.x + v.y + v.z + v.w;
+}
+
 __device__ __forceinline__ CandList cand_list(const int* cnt4, int chunk, bool through_l2) {
   CandList L;
   L.qcap = chunk / 4;

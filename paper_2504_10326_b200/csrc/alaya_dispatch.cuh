@@ -36,6 +36,7 @@ struct Stages {
       if (per_sm < 1) per_sm = 1;
     }
     const long blocks = std::min<long>((tasks + kWarps - 1) / kWarps, (long)per_sm * num_sms());
+    // primary ticket; counters[7] (overflow items) and the heavy flags come from the scan
     if (cudaMemsetAsync(ws.counters, 0, sizeof(int), st) != cudaSuccess) return cuda_check("memset");
     attend_kernel<T, D, G><<<(unsigned)blocks, kThreads, 0, st>>>(bt, q, smax, ws, want_values);
     return cuda_check("attend_kernel");

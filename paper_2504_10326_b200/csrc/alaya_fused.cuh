@@ -49,7 +49,8 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
   // full[S], empty[S], accf[kAcc], acce[kAcc], cfull[Q], cempty[Q], bfree[2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2 * kAcc + 2 * kQueue + 2);
   int* chunk_q = reinterpret_cast<int*>(tmem_slot + 4);              // [kQueue]
-  int* s_t_all = chunk_q + kQueue;                                    // [kAttnWarps][2][32]
+  float* tmax = reinterpret_cast<float*>(chunk_q + kQueue);           // [3][4][G]
+  int* s_t_all = reinterpret_cast<int*>(tmax + 3 * 4 * G);            // [kAttnWarps][2][32]
   float* s_w_all = reinterpret_cast<float*>(s_t_all + kAttnWarps * 64);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
   } else if (warp < kScanWarps) {
     // ===================== scan epilogue (warps 2..5) =====================
     const int quarter = warp & 3;
-    int acc = 0, slot = 0;
+    int acc = 0, slot = 0, tcount = 0;
     uint32_t aphase = 0, qphase = 0;
     for (;;) {
       mbar_wait(cfull_bar(slot), qphase);
@@ -174,7 +175,8 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
       if (++slot == kQueue) { slot = 0; qphase ^= 1; }
       if (c < 0) break;
       int b, h;
-      epilogue_chunk<G, NP>(bt, ws, c, quarter, lane, tmem_base, accf0, acce0, acc, aphase, b, h);
+      epilogue_chunk<G, NP>(bt, ws, c, quarter, lane, tmem_base, accf0, acce0, acc, aphase, b, h,
+                            tmax, tcount);
       __threadfence();  // this warp's candidates, counts and max are visible GPU-wide ...
       __syncwarp();
       if (lane == 0) atomicAdd(&group_done[b * bt.Hkv + h], 1);  // ... before its group count
@@ -185,7 +187,17 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
     int(*s_t)[32] = reinterpret_cast<int(*)[32]>(s_t_all + aw * 64);
     float(*s_w)[32] = reinterpret_cast<float(*)[32]>(s_w_all + aw * 64);
     const int nwin = bt.B * bt.Hq;
-    const int ntasks = nwin + bt.total_chunks * G;
+    const int npairs = bt.total_chunks * G;
+    const int ntasks = nwin + npairs;
+    auto wait_group = [&](int c) {
+      int b, h, ci;
+      decode_chunk(bt, c, b, h, ci);
+      if (lane == 0) {  // every epilogue warp of every chunk of the group published
+        const int* gd = group_done + b * bt.Hkv + h;
+        while (ld_acquire(gd) < 4 * bt.s[b].nch) __nanosleep(200);
+      }
+      __syncwarp();
+    };
     for (;;) {
       int task = 0;
       if (lane == 0) task = atomicAdd(&ws.counters[0], 1);
@@ -195,16 +207,9 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
         win_task<__nv_bfloat16, 128, G>(bt, q, ws, task, lane);
         continue;
       }
-      const int st = task - nwin;
-      const int c = st / G;
-      int b, h, ci;
-      decode_chunk(bt, c, b, h, ci);
-      if (lane == 0) {  // every epilogue warp of every chunk of the group published
-        const int* gd = group_done + b * bt.Hkv + h;
-        while (ld_acquire(gd) < 4 * bt.s[b].nch) __nanosleep(200);
-      }
-      __syncwarp();
-      sel_task_pipe<__nv_bfloat16, 128, G, true>(bt, nullptr, ws, st, lane, s_t, s_w, true);
+      const size_t cj = task - nwin;
+      wait_group((int)cj / G);
+      sel_task_pipe<__nv_bfloat16, 128, G, true>(bt, nullptr, ws, cj, 0, 4, lane, s_t, s_w, true);
     }
   }
   fence_before();
@@ -218,7 +223,8 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
 inline size_t fused_smem_bytes(int G, int kStages) {
   const int NP = (3 * G <= 16) ? 16 : 32;
   return 1024 + (size_t)kStages * tc::kTileBytes + 2 * 2 * NP * 128 +
-         8 * (2 * kStages + 2 * tc::kAcc + 2 * kQueue + 2) + 16 + 4 * kQueue + kAttnWarps * 64 * 8 + 64;
+         8 * (2 * kStages + 2 * tc::kAcc + 2 * kQueue + 2) + 16 + 4 * kQueue + 3 * 4 * G * 4 +
+         kAttnWarps * 64 * 8 + 64;
 }
 
 }  // namespace fused

@@ -157,18 +157,14 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
   }
   __syncthreads();
   const size_t cbase = (size_t)blockIdx.x * G;
+  const int quarter = warp >> 1;  // sub-list = position quarter (warps 2k, 2k+1)
 #pragma unroll
   for (int j = 0; j < G; ++j) {
     const float th = thr[j];
-    int off = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      int cw = wc[w * G + j];
-      off += (w < warp) ? cw : 0;
-      tot += cw;
-    }
-    int* oi = ws.cidx + (cbase + j) * chunk;
-    float* os = ws.cscore + (cbase + j) * chunk;
+    const int off0 = (warp & 1) ? wc[(warp - 1) * G + j] : 0;
+    int off = off0;
+    int* oi = ws.cidx + (cbase + j) * chunk + quarter * (chunk / 4);
+    float* os = ws.cscore + (cbase + j) * chunk + quarter * (chunk / 4);
     if (cntj[j] > 0) {
       for (int r = 0; r < seg; r += 32) {
         int pos = sbeg + r + lane;
@@ -184,7 +180,13 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
         off += __popc(bal);
       }
     }
-    if (tid < 4) ws.cnt[(cbase + j) * 4 + tid] = tid == 0 ? tot : 0;
+    if (tid < 4) ws.cnt[(cbase + j) * 4 + tid] = wc[(2 * tid) * G + j] + wc[(2 * tid + 1) * G + j];
+    if (tid == 4) {
+      int tot = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) tot += wc[w * G + j];
+      publish_pair(bt, ws, cbase + j, tot);
+    }
   }
 }
 
@@ -228,11 +230,13 @@ __device__ __forceinline__ void hw_dot_rows(const T* const (&rows)[kWinU], const
 // L2 = true reads inputs produced by other SMs in the same launch (__ldcg).
 template <typename T, int D, int G, bool L2>
 __device__ __forceinline__ void sel_task_pipe(const Batch& bt, const float* __restrict__ smax_ext,
-                                              const Ws& ws, int st, int lane, int (*s_t)[32],
-                                              float (*s_w)[32], bool want_values) {
+                                              const Ws& ws, size_t cj, int qb, int qe, int lane,
+                                              int (*s_t)[32], float (*s_w)[32], bool want_values) {
   constexpr int DPL = D / 16, U = kGatherU;
   const int hl = lane & 15, half = lane >> 4;
-  const int c = st / G, j = st - c * G;
+  // sub-lists [qb, qe) of pair cj = (chunk c, head j) as one virtual list; the
+  // primary task (qb = 0) writes slot cj, an overflow task (qb > 0) slot cj*4+qb
+  const int c = (int)cj / G, j = (int)cj - c * G;
   int b, h, ci;
   decode_chunk(bt, c, b, h, ci);
   const KSeq& s = bt.s[b];
@@ -243,11 +247,10 @@ __device__ __forceinline__ void sel_task_pipe(const Batch& bt, const float* __re
                               : dec_max(L2 ? __ldcg(&ws.gmax[b * bt.Hq + qh]) : ws.gmax[b * bt.Hq + qh]);
   const float th = smax - bt.beta;
   const float k2 = bt.inv_sqrt_d * kLog2e;
-  const size_t cj = (size_t)c * G + j;
-  const CandList L = cand_list(ws.cnt + cj * 4, chunk, L2);
+  const CandList L = cand_range(ws.cnt + cj * 4, qb, qe, chunk, L2);
   const int nc = L.total();
-  int* ci_ = ws.cidx + cj * chunk;
-  const float* cs_ = ws.cscore + cj * chunk;
+  int* ci_ = ws.cidx + cj * chunk + qb * (chunk / 4);
+  const float* cs_ = ws.cscore + cj * chunk + qb * (chunk / 4);
   auto ldi = [&](int i) { return L2 ? __ldcg(ci_ + L.phys(i)) : ci_[L.phys(i)]; };
   auto lds = [&](int i) { return L2 ? __ldcg(cs_ + L.phys(i)) : cs_[L.phys(i)]; };
   const T* vb = reinterpret_cast<const T*>(s.v) + (size_t)h * s.hs + (size_t)t0 * D + hl * DPL;
@@ -326,16 +329,18 @@ __device__ __forceinline__ void sel_task_pipe(const Batch& bt, const float* __re
     ns_cur = ns_nxt;
   }
   lsum = warp_sum(lsum);
+  const bool ovl = qb > 0;
+  const size_t slot = ovl ? cj * 4 + qb : cj;
   if (lane == 0) {
-    ws.selcnt[cj] = sel_tot;
-    ws.retcnt[cj] = ret_tot;
-    if (want_values) ws.part_l[cj] = lsum;
+    (ovl ? ws.ovl_sel : ws.selcnt)[slot] = sel_tot;
+    (ovl ? ws.ovl_ret : ws.retcnt)[slot] = ret_tot;
+    if (want_values) (ovl ? ws.ovl_l : ws.part_l)[slot] = lsum;
   }
   if (want_values) {
 #pragma unroll
     for (int e = 0; e < DPL; ++e) acc[e] += __shfl_xor_sync(kFull, acc[e], 16);
     if (half == 0) {
-      float* pa = ws.part_acc + cj * D + hl * DPL;
+      float* pa = (ovl ? ws.ovl_acc : ws.part_acc) + slot * D + hl * DPL;
 #pragma unroll
       for (int e = 0; e < DPL; ++e) pa[e] = acc[e];
     }
@@ -433,18 +438,31 @@ __global__ void __launch_bounds__(kThreads, 2)
   __shared__ float s_w[kWarps][2][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwin = want_values ? bt.B * bt.Hq : 0;
-  const int ntasks = nwin + bt.total_chunks * G;
-  for (;;) {  // dynamic tickets: window tasks first, then (chunk, head) tasks
+  const int npairs = bt.total_chunks * G;
+  // + overflow items published by the scan (none without chunks: no scan ran)
+  const int ntasks = nwin + npairs + (npairs ? ws.counters[7] : 0);
+  for (;;) {  // window tasks, (chunk, head) pairs, then heavy pairs' sub-lists 1..3
     int task = 0;
     if (lane == 0) task = atomicAdd(&ws.counters[0], 1);
     task = __shfl_sync(kFull, task, 0);
     if (task >= ntasks) break;
     if (task < nwin) {
       win_task<T, D, G>(bt, q, ws, task, lane);
-    } else {
-      sel_task_pipe<T, D, G, false>(bt, smax_ext, ws, task - nwin, lane, s_t[warp], s_w[warp],
-                                    want_values != 0);
+      continue;
     }
+    int qb = 0, qe;
+    size_t cj;
+    if (task < nwin + npairs) {
+      cj = task - nwin;
+      qe = ws.heavy[cj] ? 1 : 4;  // primary: whole pair, or sub-list 0 of a heavy pair
+    } else {
+      const int item = ws.ovlist[task - nwin - npairs];
+      cj = (size_t)(item >> 2);
+      qb = item & 3;
+      qe = qb + 1;
+    }
+    sel_task_pipe<T, D, G, false>(bt, smax_ext, ws, cj, qb, qe, lane, s_t[warp], s_w[warp],
+                                  want_values != 0);
   }
 }
 
@@ -477,18 +495,38 @@ __global__ void __launch_bounds__(kThreads)
   float lb = 0.f;
   int nsel = 0;
   for (int c = warp; c < s.nch; c += kWarps * U) {
-    float v[U][DL];
+    float v[U][DL], pl[U];
+    int tot[U], ps[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < U; ++u) {  // issue every load of the batch first
       const int cc = c + u * kWarps;
+      const size_t cj = (size_t)(c0 + cc) * G + j;
+      tot[u] = cc < s.nch ? ws.heavy[cj] : 0;
+      pl[u] = cc < s.nch ? ws.part_l[cj] : 0.f;
+      ps[u] = cc < s.nch ? ws.selcnt[cj] : 0;
 #pragma unroll
       for (int k = 0; k < DL; ++k) {
         const int e = lane + 32 * k;
-        v[u][k] = (cc < s.nch && e < D) ? ws.part_acc[((size_t)(c0 + cc) * G + j) * D + e] : 0.f;
+        v[u][k] = (cc < s.nch && e < D) ? ws.part_acc[cj * D + e] : 0.f;
       }
-      if (lane == 0 && cc < s.nch) {
-        lb += ws.part_l[(size_t)(c0 + cc) * G + j];
-        nsel += ws.selcnt[(size_t)(c0 + cc) * G + j];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int cc = c + u * kWarps;
+      const size_t cj = (size_t)(c0 + cc) * G + j;
+      if (cc < s.nch && tot[u]) {  // overflow sub-lists of a heavy pair
+        for (int sq = 1; sq < 4; ++sq) {
+#pragma unroll
+          for (int k = 0; k < DL; ++k) {
+            const int e = lane + 32 * k;
+            if (e < D) v[u][k] += ws.ovl_acc[(cj * 4 + sq) * D + e];
+          }
+          if (lane == 0) { lb += ws.ovl_l[cj * 4 + sq]; nsel += ws.ovl_sel[cj * 4 + sq]; }
+        }
+      }
+      if (lane == 0) {
+        lb += pl[u];
+        nsel += ps[u];
       }
     }
 #pragma unroll
@@ -578,21 +616,31 @@ __global__ void __launch_bounds__(kThreads) window_lb_kernel(const __grid_consta
   for (int k = 0; k < DL; ++k) qr[k] = lane + 32 * k < D ? q[(size_t)row * D + lane + 32 * k] : 0.f;
   const T* kb = reinterpret_cast<const T*>(s.k) + (size_t)h * s.hs;
   float lb = -INFINITY;
-  for (int r = 0; r < R; ++r) {
-    const T* kr = kb + (size_t)(r < na ? a0 + r : b0 + r - na) * D;
-    float a = 0.f, mag = 0.f;
+  constexpr int RU = 8;  // rows in flight
+  for (int r0 = 0; r0 < R; r0 += RU) {
+    float x[RU][DL];
 #pragma unroll
-    for (int k = 0; k < DL; ++k) {
-      const int e = lane + 32 * k;
-      if (e < D) {
-        const float x = to_f(kr[e]);
-        a = fmaf(qr[k], x, a);
-        mag = fmaf(fabsf(qr[k]), fabsf(x), mag);
+    for (int u = 0; u < RU; ++u) {
+      const int r = r0 + u;
+      const T* kr = kb + (size_t)(r < na ? a0 + r : b0 + r - na) * D;
+#pragma unroll
+      for (int k = 0; k < DL; ++k) {
+        const int e = lane + 32 * k;
+        x[u][k] = (r < R && e < D) ? to_f(kr[e]) : 0.f;
       }
     }
-    a = warp_sum(a);
-    mag = warp_sum(mag);
-    lb = fmaxf(lb, a - 1e-3f * (mag + 1.f));  // margin covers any scan/score rounding
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      float a = 0.f, mag = 0.f;
+#pragma unroll
+      for (int k = 0; k < DL; ++k) {
+        a = fmaf(qr[k], x[u][k], a);
+        mag = fmaf(fabsf(qr[k]), fabsf(x[u][k]), mag);
+      }
+      a = warp_sum(a);
+      mag = warp_sum(mag);
+      if (r0 + u < R) lb = fmaxf(lb, a - 1e-3f * (mag + 1.f));  // margin covers score rounding
+    }
   }
   if (lane == 0 && lb > -INFINITY) atomicMax(&ws.lbu[row], enc_max(lb));
 }

@@ -146,7 +146,7 @@ template <int G, int NP>
 __device__ __forceinline__ void epilogue_chunk(const Batch& bt, const Ws& ws, int c, int quarter,
                                                int lane, uint32_t tmem_base, uint32_t accf0,
                                                uint32_t acce0, int& acc, uint32_t& aphase,
-                                               int& b, int& h) {
+                                               int& b, int& h, float* tmax, int& tcount) {
   int ci;
   decode_chunk(bt, c, b, h, ci);
   const int chunk = bt.chunk;
@@ -172,19 +172,30 @@ __device__ __forceinline__ void epilogue_chunk(const Batch& bt, const Ws& ws, in
     if (lane == 0) mbar_arrive(acce0 + 8u * acc);
     aphase ^= 1u << acc;
     acc = (acc + 1) % kAcc;
-    if (bt.dbg & 2) continue;
     const int row = tl * kTileKeys + quarter * 32 + lane;
     const bool ok = row < valid;
+    // tile max over all 128 rows (one named barrier among the 4 epilogue warps;
+    // tmax is double-buffered by tile parity): a 32-row warp max alone misses
+    // the query's cluster often enough to bloat the candidate superset
+    float sc[G];
+    const int tb = (tcount++) & 1;
 #pragma unroll
     for (int j = 0; j < G; ++j) {
-      const float sc = ok ? v[j] + (v[G + j] + v[2 * G + j]) : -INFINITY;
-      run[j] = fmaxf(run[j], warp_max(sc));
-      const bool pass = ok && sc >= run[j] - bt.beta;
+      sc[j] = ok ? v[j] + (v[G + j] + v[2 * G + j]) : -INFINITY;
+      const float m = warp_max(sc[j]);
+      if (lane == 0) tmax[(tb * 4 + quarter) * G + j] = m;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) run[j] = fmaxf(run[j], tmax[(tb * 4 + qq) * G + j]);
+      const bool pass = ok && sc[j] >= run[j] - bt.beta;
       const unsigned bal = __ballot_sync(kFull, pass);
       if (pass) {
         const int o = qoff + cnt[j] + __popc(bal & lanemask_lt());
         ws.cidx[(cbase + j) * chunk + o] = row;
-        ws.cscore[(cbase + j) * chunk + o] = sc;
+        ws.cscore[(cbase + j) * chunk + o] = sc[j];
       }
       cnt[j] += __popc(bal);
     }
@@ -195,8 +206,16 @@ __device__ __forceinline__ void epilogue_chunk(const Batch& bt, const Ws& ws, in
       if (j == lane) {
         atomicMax(&ws.gmax[b * bt.Hq + h * G + j], enc_max(run[j]));
         ws.cnt[(cbase + j) * 4 + quarter] = cnt[j];
+        tmax[8 * G + quarter * G + j] = __int_as_float(cnt[j]);  // pair totals via smem
       }
     }
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (quarter == 0 && lane < G) {
+    int tot = 0;
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) tot += __float_as_int(tmax[8 * G + qq * G + lane]);
+    publish_pair(bt, ws, cbase + lane, tot);
   }
 }
 
@@ -224,6 +243,7 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 3 : (kStages <= 3 
   uint64_t* bars = reinterpret_cast<uint64_t*>(b_buf + 2 * kBBytes);
   // full[kStages], empty[kStages], accf[kAcc], acce[kAcc], bfree[2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2 * kAcc + 2);
+  float* tmax = reinterpret_cast<float*>(tmem_slot + 4);  // [2][4][G] tile maxima + [4][G] counts
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar0 = smem_u32(bars);
@@ -327,11 +347,12 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 3 : (kStages <= 3 
   } else {
     // ===================== epilogue (warps 2..5) =====================
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    int acc = 0;
+    int acc = 0, tcount = 0;
     uint32_t aphase = 0;
     for (int c = blockIdx.x; c < bt.total_chunks; c += gridDim.x) {
       int b, h;
-      epilogue_chunk<G, NP>(bt, ws, c, quarter, lane, tmem_base, accf0, acce0, acc, aphase, b, h);
+      epilogue_chunk<G, NP>(bt, ws, c, quarter, lane, tmem_base, accf0, acce0, acc, aphase, b, h,
+                            tmax, tcount);
     }
   }
   fence_before();
@@ -344,7 +365,8 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 3 : (kStages <= 3 
 
 inline size_t tc_smem_bytes(int G, int kStages) {
   const int NP = (3 * G <= 16) ? 16 : 32;
-  return 1024 + (size_t)kStages * kTileBytes + 2 * 2 * NP * 128 + 8 * (2 * kStages + 2 * kAcc + 2) + 64;
+  return 1024 + (size_t)kStages * kTileBytes + 2 * 2 * NP * 128 + 8 * (2 * kStages + 2 * kAcc + 2) + 16 +
+         3 * 4 * G * 4 + 64;
 }
 
 }  // namespace tc

@@ -180,6 +180,16 @@ class Call:
         v = self.ws[off:off + 8].view(torch.int32).tolist()
         return int(v[0]), int(v[1])
 
+    def candidate_counts(self, chunk: int) -> torch.Tensor:
+        """Candidate-superset sizes of the last scan: int32 ``[chunks, G, 4]`` (diagnostics;
+        ``chunk`` = the tokens per work chunk the call used)."""
+        p = self.lib.alaya_ws_candidate_counts(ctypes.byref(self.params), self.seqs, self.B,
+                                               self.ws.data_ptr())
+        off = p - self.ws.data_ptr()
+        g = self.params.n_query_heads // self.params.n_kv_heads
+        nch = sum((self.seqs[i].n + chunk - 1) // chunk for i in range(self.B))
+        return self.ws[off:off + 16 * g * nch * self.params.n_kv_heads].view(torch.int32).view(-1, g, 4)
+
     def status(self) -> int:
         """Device status word of the last dipr_attention (synchronises)."""
         return int(self.ws[:4].view(torch.int32).item())
