@@ -66,8 +66,9 @@ def _seqs(n=131072, B=1):
 def test_workspace_sizing_is_host_only():
     lib = _lib.load()
     nb = lib.alaya_workspace_bytes(ctypes.byref(_params()), _seqs(), 1)
-    # candidates (idx+score) for every (token, q head) dominate: 8 B * n * Hq
-    assert 8 * 131072 * 32 <= nb < 8 * 131072 * 32 * 1.2
+    # candidates (idx+score) for every (token, q head) plus the chunk partials:
+    # between 1x and 2x of 8 B * n * Hq, far below the K slab (256 B * n * Hkv)
+    assert 8 * 131072 * 32 <= nb < 2 * 8 * 131072 * 32
     assert lib.alaya_workspace_bytes(ctypes.byref(_params(n_query_heads=30)), _seqs(), 1) == 0
 
 
