@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: warmup + steps only, no side measurements")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--check", action="store_true",
+                    help="N>1: generate identical full contexts on every rank (small sizes) and "
+                         "compare the sharded layer-0 output with the unsharded kernels")
     return ap.parse_args()
 
 
@@ -246,10 +249,18 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # ALAYA_BENCH_SHARE_GPU=1: validation of the multi-rank path on ONE GPU (all
+    # ranks on cuda:0, gloo collectives staged through host memory); never a result
+    share = os.environ.get("ALAYA_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     dtype = torch.bfloat16 if a.kv_dtype == "bfloat16" else torch.float32
     esize = 2 if dtype == torch.bfloat16 else 4
     L, Hq, Hkv, d = a.layers, a.hq, a.hkv, a.dim
@@ -267,7 +278,13 @@ def main():
     V = torch.empty_like(K)
     for l in range(L):
         for b in range(B):
-            K[l, b], V[l, b] = gen_slab(torch, centers, n_loc, Hkv, d, dtype, g, dev)
+            if a.check:  # identical full context on every rank, this rank keeps its shard
+                gf = torch.Generator(device=dev).manual_seed(104729 * (a.seed + 1) + 131 * l + b)
+                kf, vf = gen_slab(torch, centers, a.ctx, Hkv, d, dtype, gf, dev)
+                K[l, b], V[l, b] = kf[:, off:off + n_loc], vf[:, off:off + n_loc]
+                del kf, vf
+            else:
+                K[l, b], V[l, b] = gen_slab(torch, centers, n_loc, Hkv, d, dtype, g, dev)
     steps_total = a.warmup + a.steps
     cap = a.window_rows + steps_total + 1
     last_rank = rank == world - 1
@@ -298,9 +315,10 @@ def main():
     def step(s):
         w = a.window_rows + s + 1
         for l in range(L):
-            if kv_ring_owner:  # Session.update: append this token's K/V
-                WK[l, :, :, w - 1] = KN[s, l]
-                WV[l, :, :, w - 1] = VN[s, l]
+            if kv_ring_owner or a.check:  # Session.update: append this token's K/V
+                WK[l, :, :, w - 1] = KN[s, l]  # (--check: every rank mirrors the ring so
+                WV[l, :, :, w - 1] = VN[s, l]  # rank 0 can run the unsharded reference)
+            if kv_ring_owner:
                 calls[l].set_window_rows(w)
             if world == 1:
                 calls[l].dipr_attention(Q[s, l], out=out[l])
@@ -327,9 +345,27 @@ def main():
             dist.barrier()
     ms = ev0.elapsed_time(ev1) / a.steps
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device=dev if not share else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    sharded_check = None
+    if world > 1 and a.check:
+        # one more sharded layer-0 step vs the unsharded kernels on the full context
+        s_last = a.warmup + a.steps - 1
+        o_sh = sharded_attention(stages[0], Q[s_last, 0]).clone()
+        if rank == 0:
+            wf = a.window_rows + a.warmup + a.steps
+            full = []
+            for b in range(B):
+                gf = torch.Generator(device=dev).manual_seed(104729 * (a.seed + 1) + 131 * 0 + b)
+                kf, vf = gen_slab(torch, centers, a.ctx, Hkv, d, dtype, gf, dev)
+                full.append(engine.SeqView(k=kf, v=vf, n=a.ctx, wk=WK[0, b], wv=WV[0, b], w=wf))
+            params1 = engine.make_params(Hq, Hkv, d, dtype, a.beta, 16, 64)
+            c1 = engine.Call(full, params1, dtype, dev,
+                             ws=torch.empty(1, dtype=torch.uint8, device=dev))
+            o_ref = c1.dipr_attention(Q[s_last, 0])
+            err = float(((o_sh - o_ref).norm() / o_ref.norm()).item())
+            sharded_check = {"layer0_norm_rel_err_vs_unsharded": err, "ok": err <= 1e-5}
     qheads = B * L * Hq
     value = qheads / (ms / 1e3)
     if a.profile:
@@ -433,6 +469,7 @@ def main():
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": a.steps * L * (3 if world == 1 else 4),
                 "clocks": sampler.summary(), "parity": parity, "stats": stats,
+                "sharded_check": sharded_check,
                 "gen_seconds": round(t_gen, 2)}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -71,17 +71,29 @@ class EngineStages:
         return engine.merge_partials(parts, self.dim)
 
 
+def _staged(t: torch.Tensor, group) -> tuple[torch.Tensor, bool]:
+    """gloo cannot run these collectives on CUDA tensors: stage through host."""
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        return t.cpu(), True
+    return t, False
+
+
 def sharded_attention(stages: LocalStages, q: torch.Tensor, group=None) -> torch.Tensor:
     """One decode step of one layer over sequence-sharded KV -> ``[B, Hq, d]``
     (identical on every rank)."""
     world = dist.get_world_size(group)
     smax = stages.scan(q)
-    dist.all_reduce(smax, op=dist.ReduceOp.MAX, group=group)
-    part = stages.attend(q, smax)
-    part = part.contiguous()
-    parts = torch.empty((world * part.shape[0],) + tuple(part.shape[1:]), dtype=part.dtype,
-                        device=part.device)
-    dist.all_gather_into_tensor(parts, part, group=group)
+    sm, moved = _staged(smax, group)
+    dist.all_reduce(sm, op=dist.ReduceOp.MAX, group=group)
+    if moved:
+        smax.copy_(sm)
+    part = stages.attend(q, smax).contiguous()
+    pt, moved = _staged(part, group)
+    parts = torch.empty((world * pt.shape[0],) + tuple(pt.shape[1:]), dtype=pt.dtype,
+                        device=pt.device)
+    dist.all_gather_into_tensor(parts, pt, group=group)
+    if moved:
+        parts = parts.to(part.device)
     out = stages.merge(parts.view((world,) + tuple(part.shape)))
     return out.view(q.shape[0], q.shape[1], -1)
 
