@@ -109,6 +109,8 @@ int build_batch(const alaya_params* p, const alaya_seq* seqs, int B, Batch* bt) 
   {  // attend task split threshold; ALAYA_SPLIT overrides (diagnostics)
     const char* e = getenv("ALAYA_SPLIT");
     bt->split = (e && *e) ? atoi(e) : std::max(256, chunk / 4);
+    const char* sd = getenv("ALAYA_SEED");  // diagnostics: 0 = no running-max seed
+    bt->seed = (sd && *sd) ? atoi(sd) : 1;
   }
   int cb = 0;
   for (int b = 0; b < B; ++b) {
@@ -236,7 +238,8 @@ int prepare(const alaya_params* p, const alaya_seq* seqs, int B, void* d_ws, siz
 int run_scan(Call& c, const float* d_q) {
   const size_t rows = (size_t)c.bt.B * c.bt.Hq;
   (void)rows;
-  if (cudaMemsetAsync(c.ws.gmax, 0, c.L.zero_bytes, c.stream) != cudaSuccess) return cuda_check("memset");
+  int rc = c.st.prep(c.bt, d_q, c.ws, c.stream);  // zeroes the header, seeds the max
+  if (rc) return rc;
   if (c.bt.block_filter) {
     const int rc = c.st.filter(c.bt, d_q, c.ws, c.stream);
     if (rc) return rc;
@@ -323,16 +326,15 @@ int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch
   if (!d_q || !d_out) return fail(ALAYA_ERR_ARG, "null q/out");
   for (int b = 0; b < batch; ++b)
     if (seqs[b].prefix_len + seqs[b].w == 0) return fail(ALAYA_ERR_ARG, "attention on an empty session");
-  if (cudaMemsetAsync(c.ws.status, 0, 4, c.stream) != cudaSuccess) return cuda_check("memset");
   if (c.use_tc && fused_enabled()) {  // scan + attend in one persistent kernel
-    if (cudaMemsetAsync(c.ws.gmax, 0, c.L.zero_bytes, c.stream) != cudaSuccess) return cuda_check("memset");
+    if ((rc = c.st.prep(c.bt, d_q, c.ws, c.stream))) return rc;
     if (c.bt.block_filter && (rc = c.st.filter(c.bt, d_q, c.ws, c.stream))) return rc;
     c.bt.split = 0x7fffffff;  // the fused kernel runs whole (chunk, head) pairs
     if ((rc = launch_tc_fused(c.bt, c.seqs, d_q, c.ws, c.stream))) return rc;
     return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);
   }
-  if ((rc = run_scan(c, d_q))) return rc;
-  if ((rc = c.st.attend(c.bt, d_q, nullptr, c.ws, 1, c.stream))) return rc;
+  if ((rc = run_scan(c, d_q))) return rc;  // prep zeroed the status word and the ticket
+  if ((rc = c.st.attend(c.bt, d_q, nullptr, c.ws, 1, c.stream, 0))) return rc;
   return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);
 }
 
@@ -355,7 +357,7 @@ int alaya_attend(const alaya_params* p, const alaya_seq* seqs, int batch, const 
   int rc = prepare(p, seqs, batch, d_ws, ws_bytes, stream, &c);
   if (rc) return rc;
   if (!d_q || !d_smax) return fail(ALAYA_ERR_ARG, "null q/smax");
-  if ((rc = c.st.attend(c.bt, d_q, d_smax, c.ws, want_values ? 1 : 0, c.stream))) return rc;
+  if ((rc = c.st.attend(c.bt, d_q, d_smax, c.ws, want_values ? 1 : 0, c.stream, 1))) return rc;
   if (!want_values || !d_part) return ALAYA_OK;
   return c.st.combine(c.bt, d_smax, c.ws, nullptr, d_part, nullptr, c.stream);
 }

@@ -45,6 +45,7 @@ struct Batch {
   int32_t dbg;  // diagnostics only (ALAYA_TC_DBG): bit0 no L2 hint, bit1 no epilogue math, bit2 no MMA
   int32_t block_filter;
   int32_t split;  // attend task split threshold (candidates per (chunk, head) pair)
+  int32_t seed;   // prep_kernel seeds the running max from sampled keys
 };
 
 // Workspace pointers (device), carved from the caller's buffer.
@@ -72,6 +73,14 @@ struct Ws {
   unsigned long long* keep;  // [chunks] block-filter masks: bit t = 128-key tile t of the chunk kept
   uint32_t* lbu;    // [B*Hq] encoded lower bound of the DIPR max (block filter); zeroed with gmax
 };
+
+// Programmatic dependent launch: a kernel launched with the PDL attribute may
+// start while its predecessor on the stream is still running; pdl_wait()
+// blocks until the predecessor grid has completed and its writes are visible
+// (no-op without the attribute). pdl_trigger() lets this grid's dependent
+// launch early (its CTAs then park in their own pdl_wait()).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t enc_max(float f) {
   uint32_t u = __float_as_uint(f);

@@ -13,6 +13,28 @@ int fail(int code, const char* fmt, ...);
 int num_sms();
 int cuda_check(const char* what);
 
+bool pdl_enabled();
+
+// Launch with the programmatic-dependent-launch attribute (ALAYA_PDL=0 turns
+// it off). Every kernel launched this way calls pdl_wait() before touching
+// data written by earlier work on the stream.
+template <typename... KArgs, typename... Args>
+int launch_pdl(const char* what, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+               cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  return cuda_check(what);
+}
+
 inline size_t scan_smem(const Batch& bt) {
   return (size_t)bt.G * bt.chunk * 4 + kWarps * bt.G * 4 + bt.G * 4 + kWarps * bt.G * 4;
 }
@@ -23,11 +45,14 @@ struct Stages {
     if (bt.total_chunks == 0) return ALAYA_OK;
     size_t sm = scan_smem(bt);
     cudaFuncSetAttribute(scan_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    scan_kernel<T, D, G><<<bt.total_chunks, kThreads, sm, st>>>(bt, q, ws);
-    return cuda_check("scan_kernel");
+    return launch_pdl("scan_kernel", scan_kernel<T, D, G>, bt.total_chunks, kThreads, sm, st, bt, q, ws);
   }
+  static int prep(const Batch& bt, const float* q, const Ws& ws, cudaStream_t st) {
+    return launch_pdl("prep_kernel", prep_kernel<T, D, G>, bt.B * bt.Hkv, kThreads, 0, st, bt, q, ws);
+  }
+  // zero_ticket = 0: the ticket was zeroed by prep_kernel in this call
   static int attend(const Batch& bt, const float* q, const float* smax, const Ws& ws,
-                    int want_values, cudaStream_t st) {
+                    int want_values, cudaStream_t st, int zero_ticket = 1) {
     const long tasks = (long)bt.total_chunks * G + (want_values ? (long)bt.B * bt.Hq : 0);
     if (tasks == 0) return ALAYA_OK;
     static int per_sm = 0;
@@ -37,9 +62,10 @@ struct Stages {
     }
     const long blocks = std::min<long>((tasks + kWarps - 1) / kWarps, (long)per_sm * num_sms());
     // primary ticket; counters[7] (overflow items) and the heavy flags come from the scan
-    if (cudaMemsetAsync(ws.counters, 0, sizeof(int), st) != cudaSuccess) return cuda_check("memset");
-    attend_kernel<T, D, G><<<(unsigned)blocks, kThreads, 0, st>>>(bt, q, smax, ws, want_values);
-    return cuda_check("attend_kernel");
+    if (zero_ticket && cudaMemsetAsync(ws.counters, 0, sizeof(int), st) != cudaSuccess)
+      return cuda_check("memset");
+    return launch_pdl("attend_kernel", attend_kernel<T, D, G>, (unsigned)blocks, kThreads, 0, st, bt, q,
+                      smax, ws, want_values);
   }
   static int filter(const Batch& bt, const float* q, const Ws& ws, cudaStream_t st) {
     if (bt.total_chunks == 0) return ALAYA_OK;
@@ -52,13 +78,13 @@ struct Stages {
   static int combine(const Batch& bt, const float* smax, const Ws& ws, float* out,
                      float* part_out, float* smax_out, cudaStream_t st) {
     const int rows = bt.B * bt.Hq;
-    combine_kernel<D, G><<<rows, kThreads, 0, st>>>(bt, smax, ws, out, part_out, smax_out);
-    return cuda_check("combine_kernel");
+    return launch_pdl("combine_kernel", combine_kernel<D, G>, rows, kThreads, 0, st, bt, smax, ws, out,
+                      part_out, smax_out);
   }
 };
 
 using ScanFn = int (*)(const Batch&, const float*, const Ws&, cudaStream_t);
-using AttendFn = int (*)(const Batch&, const float*, const float*, const Ws&, int, cudaStream_t);
+using AttendFn = int (*)(const Batch&, const float*, const float*, const Ws&, int, cudaStream_t, int);
 using FilterFn = int (*)(const Batch&, const float*, const Ws&, cudaStream_t);
 using CombineFn = int (*)(const Batch&, const float*, const Ws&, float*, float*, float*,
                           cudaStream_t);
@@ -68,12 +94,13 @@ struct StageSet {
   AttendFn attend;
   CombineFn combine;
   FilterFn filter;
+  ScanFn prep;
 };
 
 template <typename T, int D, int G>
 StageSet make_set() {
   return {&Stages<T, D, G>::scan, &Stages<T, D, G>::attend, &Stages<T, D, G>::combine,
-          &Stages<T, D, G>::filter};
+          &Stages<T, D, G>::filter, &Stages<T, D, G>::prep};
 }
 
 template <typename T, int D>

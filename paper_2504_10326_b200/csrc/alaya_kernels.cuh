@@ -42,6 +42,8 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
   float* thr = red + kWarps * G;           // [G]
   int* wc = reinterpret_cast<int*>(thr + G);  // [kWarps][G]
 
+  pdl_trigger();
+  pdl_wait();
   int b, h, ci;
   decode_chunk(bt, blockIdx.x, b, h, ci);
   const KSeq& s = bt.s[b];
@@ -436,6 +438,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                   const float* __restrict__ smax_ext, Ws ws, int want_values) {
   __shared__ int s_t[kWarps][2][32];
   __shared__ float s_w[kWarps][2][32];
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwin = want_values ? bt.B * bt.Hq : 0;
   const int npairs = bt.total_chunks * G;
@@ -483,6 +487,8 @@ __global__ void __launch_bounds__(kThreads)
   __shared__ float red[kWarps][D];
   __shared__ float redl[kWarps];
   __shared__ int redn[kWarps];
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int row = blockIdx.x;
   const int b = row / bt.Hq, qh = row - b * bt.Hq;
@@ -643,6 +649,88 @@ __global__ void __launch_bounds__(kThreads) window_lb_kernel(const __grid_consta
     }
   }
   if (lane == 0 && lb > -INFINITY) atomicMax(&ws.lbu[row], enc_max(lb));
+}
+
+// Per-call preparation (replaces a memset of the workspace header): zero the
+// tickets, group counters, block-filter bounds and status word, and SEED the
+// running max of every (sequence, q head) with a lower bound of its DIPR max:
+// the scores of kPrepSamples evenly spaced base keys of this shard, minus a
+// rounding margin (so the seed is below what the scan computes for the same
+// keys). The scan raises the max to the exact value; seeding only tightens
+// its early candidate bound (clustered / locality-ordered prefixes would
+// otherwise emit whole chunks as candidates before any chunk max is known).
+// One CTA per (sequence, kv head).
+constexpr int kPrepSamples = 64;
+
+template <typename T, int D, int G>
+__global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ Batch bt,
+                                                        const float* __restrict__ q, Ws ws) {
+  constexpr int DL = (D + 31) / 32;
+  __shared__ float red[kWarps][G];
+  pdl_trigger();
+  pdl_wait();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b = blockIdx.x / bt.Hkv, h = blockIdx.x - b * bt.Hkv;
+  const KSeq& s = bt.s[b];
+  if (blockIdx.x == 0 && threadIdx.x < 16) {
+    ws.counters[threadIdx.x] = 0;
+    if (threadIdx.x == 0) *ws.status = 0;
+  }
+  if (threadIdx.x == 0) ws.group_done[blockIdx.x] = 0;
+  if (threadIdx.x < G) ws.lbu[b * bt.Hq + h * G + threadIdx.x] = 0u;
+  float qr[G][DL];
+#pragma unroll
+  for (int j = 0; j < G; ++j)
+#pragma unroll
+    for (int k = 0; k < DL; ++k) {
+      const int e = lane + 32 * k;
+      qr[j][k] = e < D ? __ldg(q + ((size_t)b * bt.Hq + h * G + j) * D + e) : 0.f;
+    }
+  float best[G];
+#pragma unroll
+  for (int j = 0; j < G; ++j) best[j] = -INFINITY;
+  const int S = min(s.n, kPrepSamples);
+  const T* kb = reinterpret_cast<const T*>(s.k) + (size_t)h * s.hs;
+  constexpr int RU = kPrepSamples / kWarps;  // one round of loads per warp
+  for (int i0 = warp * RU; i0 < S; i0 += kWarps * RU) {
+    float x[RU][DL];
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      const int i = i0 + u;
+      const T* kr = kb + (size_t)((int64_t)i * s.n / S) * D;
+#pragma unroll
+      for (int k = 0; k < DL; ++k) {
+        const int e = lane + 32 * k;
+        x[u][k] = (i < S && e < D) ? to_f(kr[e]) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        float a = 0.f, mag = 0.f;
+#pragma unroll
+        for (int k = 0; k < DL; ++k) {
+          a = fmaf(qr[j][k], x[u][k], a);
+          mag = fmaf(fabsf(qr[j][k]), fabsf(x[u][k]), mag);
+        }
+        a = warp_sum(a);
+        mag = warp_sum(mag);
+        if (i0 + u < S) best[j] = fmaxf(best[j], a - 1e-3f * (mag + 1.f));
+      }
+    }
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int j = 0; j < G; ++j) red[warp][j] = best[j];
+  __syncthreads();
+  if (threadIdx.x < G) {
+    float m = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) m = fmaxf(m, red[w][threadIdx.x]);
+    // no seed (0 = -inf) for an empty shard or when seeding is off
+    ws.gmax[b * bt.Hq + h * G + threadIdx.x] = (bt.seed && m > -INFINITY) ? enc_max(m) : 0u;
+  }
 }
 
 // Per chunk: representative-key lower bound (pass 0) or keep mask (pass 1).

@@ -136,6 +136,36 @@ __device__ __forceinline__ void build_b(uint8_t* bbuf, const float* __restrict__
   }
 }
 
+// Same B operand from the group's q held in registers: lane holds elements
+// idx = lane + 32*i (i < 4G) of the [G][128] block, loaded one chunk ahead so
+// the MMA warp never waits on a global load at a chunk boundary.
+template <int G>
+__device__ __forceinline__ void load_q_regs(const float* __restrict__ qg, float (&r)[4 * G], int lane) {
+#pragma unroll
+  for (int i = 0; i < 4 * G; ++i) r[i] = __ldg(qg + lane + 32 * i);
+}
+template <int G, int NP>
+__device__ __forceinline__ void build_b_regs(uint8_t* bbuf, const float (&r)[4 * G], int lane) {
+#pragma unroll
+  for (int i = 0; i < 4 * G; ++i) {
+    const int idx = lane + 32 * i;
+    const int j = idx >> 7, k = idx & 127;
+    const float x = r[i];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+    const float r1 = x - __bfloat162float(hi);
+    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+    const float r2 = r1 - __bfloat162float(mid);
+    const uint16_t parts[3] = {__bfloat16_as_ushort(hi), __bfloat16_as_ushort(mid), bf16_bits(r2)};
+    const int box = k >> 6, kk = k & 63, c16 = kk >> 3, w = kk & 7;
+#pragma unroll
+    for (int sp = 0; sp < 3; ++sp) {
+      const int n = sp * G + j;
+      const int off = box * (NP * 128) + (n >> 3) * 1024 + (n & 7) * 128 + ((c16 ^ (n & 7)) << 4) + w * 2;
+      *reinterpret_cast<uint16_t*>(bbuf + off) = parts[sp];
+    }
+  }
+}
+
 constexpr int kAcc = 4;  // TMEM accumulator buffers (MMA runs up to 4 tiles ahead)
 
 // One chunk of the scan epilogue for this warp's TMEM lane quarter (32 key
@@ -146,17 +176,18 @@ template <int G, int NP>
 __device__ __forceinline__ void epilogue_chunk(const Batch& bt, const Ws& ws, int c, int quarter,
                                                int lane, uint32_t tmem_base, uint32_t accf0,
                                                uint32_t acce0, int& acc, uint32_t& aphase,
-                                               int& b, int& h, float* tmax, int& tcount) {
+                                               int& b, int& h, float* tmax, int& tcount,
+                                               const uint32_t* pre = nullptr) {
   int ci;
   decode_chunk(bt, c, b, h, ci);
   const int chunk = bt.chunk;
   const int valid = min(chunk, bt.s[b].n - ci * chunk);
   const int ntiles = (valid + kTileKeys - 1) / kTileKeys;
-  float run[G];
+  float run[G], run0[G];
   int cnt[G];
 #pragma unroll
   for (int j = 0; j < G; ++j) {
-    run[j] = dec_max(__ldcg(&ws.gmax[b * bt.Hq + h * G + j]));
+    run[j] = run0[j] = dec_max(pre ? pre[j] : __ldcg(&ws.gmax[b * bt.Hq + h * G + j]));
     cnt[j] = 0;
   }
   const size_t cbase = (size_t)c * G;
@@ -204,7 +235,11 @@ __device__ __forceinline__ void epilogue_chunk(const Batch& bt, const Ws& ws, in
 #pragma unroll
     for (int j = 0; j < G; ++j) {
       if (j == lane) {
-        atomicMax(&ws.gmax[b * bt.Hq + h * G + j], enc_max(run[j]));
+        // run[] is the same in the 4 epilogue warps (tile maxima are shared through
+        // smem): one warp publishes, and only a max this chunk actually raised --
+        // the gmax lines are shared by every CTA of the call, so atomics queued
+        // there would stall the chunk-start reads of all of them
+        if (quarter == 0 && run[j] > run0[j]) atomicMax(&ws.gmax[b * bt.Hq + h * G + j], enc_max(run[j]));
         ws.cnt[(cbase + j) * 4 + quarter] = cnt[j];
         tmax[8 * G + quarter * G + j] = __int_as_float(cnt[j]);  // pair totals via smem
       }
@@ -270,6 +305,8 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 3 : (kStages <= 3 
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int chunk = bt.chunk;
+  pdl_trigger();
+  pdl_wait();  // gmax seeds and q come from the preceding kernels
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -305,6 +342,13 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 3 : (kStages <= 3 
     const uint32_t idesc = idesc_bf16<NP>();
     int stage = 0, acc = 0, cidx = 0, bcnt = 0;
     uint32_t phase = 0, ephase = 0, bphase = 0;
+    float qr[4 * G];
+    auto q_of = [&](int c) {
+      int b, h, ci;
+      decode_chunk(bt, c, b, h, ci);
+      return q + ((size_t)b * bt.Hq + (size_t)h * G) * 128;
+    };
+    if (blockIdx.x < bt.total_chunks) load_q_regs<G>(q_of(blockIdx.x), qr, lane);
     for (int c = blockIdx.x; c < bt.total_chunks; c += gridDim.x, ++cidx) {
       int b, h, ci;
       decode_chunk(bt, c, b, h, ci);
@@ -322,9 +366,11 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 3 : (kStages <= 3 
           // wait until the MMAs that last read this B buffer have completed
           mbar_wait(bfree0 + 8u * bi, ((bphase >> bi) & 1u) ^ 1u);
           bphase ^= 1u << bi;
-          build_b<G, NP>(bb, q + ((size_t)b * bt.Hq + (size_t)h * G) * 128, lane);
+          build_b_regs<G, NP>(bb, qr, lane);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
+          // next chunk's q: in flight while this chunk's tiles are issued
+          if (c + (int)gridDim.x < bt.total_chunks) load_q_regs<G>(q_of(c + gridDim.x), qr, lane);
         }
         mbar_wait(full_bar(stage), phase);
         fence_after();
@@ -349,10 +395,24 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 3 : (kStages <= 3 
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     int acc = 0, tcount = 0;
     uint32_t aphase = 0;
+    // the running max a chunk starts from is read one chunk ahead (any earlier
+    // value is a valid lower bound), so no chunk waits on that load
+    uint32_t pre[G];  // raw (encoded): decoded only when the chunk starts
+    auto load_pre = [&](int c) {
+      int b, h, ci;
+      decode_chunk(bt, c, b, h, ci);
+#pragma unroll
+      for (int j = 0; j < G; ++j) pre[j] = __ldcg(&ws.gmax[b * bt.Hq + h * G + j]);
+    };
+    if (blockIdx.x < bt.total_chunks) load_pre(blockIdx.x);
     for (int c = blockIdx.x; c < bt.total_chunks; c += gridDim.x) {
+      uint32_t cur[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j) cur[j] = pre[j];
+      if (c + (int)gridDim.x < bt.total_chunks) load_pre(c + gridDim.x);
       int b, h;
       epilogue_chunk<G, NP>(bt, ws, c, quarter, lane, tmem_base, accf0, acce0, acc, aphase, b, h,
-                            tmax, tcount);
+                            tmax, tcount, cur);
     }
   }
   fence_before();

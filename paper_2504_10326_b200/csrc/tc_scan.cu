@@ -52,9 +52,13 @@ int launch_s(const Batch& bt, const tc::Maps& maps, const float* q, const Ws& ws
              int ctas_per_sm) {
   const size_t sm = tc::tc_smem_bytes(G, S);
   cudaFuncSetAttribute(tc::scan_tc_kernel<G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  const int grid = std::min(bt.total_chunks, ctas_per_sm * num_sms());
-  tc::scan_tc_kernel<G, S><<<grid, tc::kThreadsTc, sm, st>>>(bt, maps, q, ws);
-  return cuda_check("scan_tc_kernel");
+  // equal chunk counts per CTA: ceil(chunks / rounds) CTAs, rounds = ceil(chunks /
+  // resident slots), so no tail round runs a fraction of the grid
+  const int slots = ctas_per_sm * num_sms();
+  const int rounds = (bt.total_chunks + slots - 1) / slots;
+  static const int balance = env_int("ALAYA_TC_BALANCE", 1);
+  const int grid = balance ? (bt.total_chunks + rounds - 1) / rounds : std::min(bt.total_chunks, slots);
+  return launch_pdl("scan_tc_kernel", tc::scan_tc_kernel<G, S>, grid, tc::kThreadsTc, sm, st, bt, maps, q, ws);
 }
 
 // Persistent CTAs per SM (ALAYA_TC_CTAS, default 3): 2 CTAs with 3-stage rings
@@ -128,6 +132,11 @@ bool tc_scan_eligible(const Batch& bt, int dtype, const alaya_seq* seqs) {
     distinct += !seen;
   }
   return distinct <= tc::kMaxMaps && encode_fn() != nullptr;
+}
+
+bool pdl_enabled() {
+  static const int on = env_int("ALAYA_PDL", 1);
+  return on != 0;
 }
 
 bool fused_enabled() {
