@@ -99,6 +99,18 @@ typedef struct {
                           * of the DIPR max). Exact: the DIPR set is unchanged. */
 } alaya_params;
 
+/* Coarse block index of one sequence's context (alaya_block_reps output):
+ * reps + h*head_stride + (blk*r + i)*dim = representative i of block blk of
+ * kv head h; the index was built over n_tokens tokens (the full imported
+ * context; a reused prefix may be shorter, index.py:206-214 then clips). */
+typedef struct {
+  const void* reps;
+  int64_t head_stride;
+  int64_t n_tokens;
+  int32_t n_blocks;
+  int32_t r;
+} alaya_block_index;
+
 #define ALAYA_MAX_BATCH 128
 #define ALAYA_PARTIAL_STRIDE(dim) ((dim) + 2) /* (m, l, acc[dim]) per query head */
 
@@ -166,6 +178,47 @@ int alaya_window_append(const alaya_params* p, const alaya_seq* seqs, int batch,
  * bounds_head_stride >= ceil(n/128)*5*dim. */
 int alaya_block_bounds(const void* d_k, int dtype, int n_heads, int64_t head_stride, int n, int dim,
                        void* d_bounds, int64_t bounds_head_stride, void* stream);
+
+/* TOP_K retrieval on the flat index (FlatIndex.top_k, index.py:60-66, as
+ * Session._retrieve uses it, store.py:314-318): per (seq, q head) the k base
+ * tokens of largest q.k (ties: smaller token id), as global ids in no
+ * particular order, into d_ids[(b*Hq+qh)*cap ...] (their fp32 scores into
+ * d_scores, nullable) with the count in d_count[b*Hq+qh] (= min(k, n)). Same workspace as alaya_dipr_attention
+ * (beta and block_filter of *p are ignored). Unsharded sequences only. */
+int alaya_topk(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q, int k,
+               int64_t* d_ids, float* d_scores, int64_t cap, int32_t* d_count, void* d_ws,
+               size_t ws_bytes, void* stream);
+
+/* BlockIndex build (build_block_index / select_representatives,
+ * index.py:217-243): for kv head h and block blk = [blk*block_size, ...) of
+ * d_k, the r keys of largest L2 norm (ties: smaller position) into
+ * d_reps[h*reps_head_stride + (blk*r + i)*dim] (K dtype); a block with fewer
+ * than r keys repeats its first representative. */
+int alaya_block_reps(const void* d_k, int dtype, int n_heads, int64_t head_stride, int n, int dim,
+                     int block_size, int r, void* d_reps, int64_t reps_head_stride, void* stream);
+
+/* TOP_K over the coarse block index (Session._retrieve, store.py:305-312 with
+ * BlockIndex.top_blocks, index.py:206-214): per (seq, q head) the k_blocks
+ * blocks of largest max-representative score (ties: smaller start), their
+ * token ranges clipped to the sequence's prefix, as global ids into
+ * d_ids/d_count like alaya_topk; the chosen block numbers and scores (no
+ * order) into d_blocks/d_block_scores [(b*Hq+qh)*k_blocks ...] (nullable).
+ * bix: host array [batch]. */
+int alaya_block_topk(const alaya_params* p, const alaya_seq* seqs, const alaya_block_index* bix,
+                     int batch, int block_size, int k_blocks, const float* d_q, int64_t* d_ids,
+                     int64_t cap, int32_t* d_count, int32_t* d_blocks, float* d_block_scores,
+                     void* stream);
+
+/* Sparse attention over explicit base ids (Session._head_attention after
+ * retrieval, store.py:268-293): ids in the base window (core.py:159-165) are
+ * dropped, PartialAttention.over(rest) is merged with the window partial
+ * (base window ids + session rows) and finalized into d_out [batch*Hq][dim].
+ * d_selected (nullable) receives the kept id count; a non-finite output sets
+ * *d_status (nullable device int) to ALAYA_ERR_NONFINITE. */
+int alaya_sparse_attention(const alaya_params* p, const alaya_seq* seqs, int batch,
+                           const float* d_q, const int64_t* d_ids, int64_t cap,
+                           const int32_t* d_count, float* d_out, int32_t* d_selected,
+                           int32_t* d_status, void* stream);
 
 /* Blocks kept / blocks considered by the block filter in the last scan on
  * this workspace: device pointer to two int32 (valid after the scan). */

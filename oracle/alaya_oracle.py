@@ -244,6 +244,124 @@ def select_representatives(block_keys: np.ndarray, r: int) -> np.ndarray:
     return block_keys[order[:r]]
 
 
+def flat_top_k(q: np.ndarray, keys: np.ndarray, k: int) -> list[int]:
+    """Exact top-k ids, scores descending, ties by smaller id -- ``index.py:60-66``."""
+    keys = np.atleast_2d(keys)
+    n = keys.shape[0]
+    if not 1 <= k <= n:
+        raise ValueError(f"k must be in [1, {n}], got {k}")
+    scores = inner_products(keys, q)
+    order = np.lexsort((np.arange(n), -scores))
+    return order[:k].tolist()
+
+
+@dataclass
+class BlockIndex:
+    """Contiguous token blocks scored by representatives -- ``index.py:195-214``."""
+
+    block_size: int
+    starts: np.ndarray
+    ends: np.ndarray
+    reps: list
+
+    @property
+    def n_blocks(self) -> int:
+        return len(self.reps)
+
+    def block_scores(self, q: np.ndarray) -> np.ndarray:
+        return np.array([inner_products(r, q).max() for r in self.reps])
+
+    def top_blocks(self, q: np.ndarray, k_blocks: int) -> list:
+        """Best ``k_blocks`` ranges by max representative score, ties by start."""
+        if not 1 <= k_blocks <= self.n_blocks:
+            raise ValueError(f"k_blocks must be in [1, {self.n_blocks}], got {k_blocks}")
+        scores = self.block_scores(q)
+        order = np.lexsort((self.starts, -scores))
+        return [(int(self.starts[i]), int(self.ends[i])) for i in order[:k_blocks]]
+
+
+def build_block_index(keys: np.ndarray, block_size: int, r: int) -> BlockIndex:
+    """Contiguous blocks + representatives -- ``index.py:231-243``."""
+    keys = np.atleast_2d(keys)
+    if block_size < 1:
+        raise ValueError("block_size must be positive")
+    n = keys.shape[0]
+    starts = np.arange(0, n, block_size, dtype=np.int64)
+    ends = np.minimum(starts + block_size, n)
+    reps = [select_representatives(keys[s:e], min(r, e - s)) for s, e in zip(starts, ends)]
+    return BlockIndex(block_size=block_size, starts=starts, ends=ends, reps=reps)
+
+
+def retrieve_top_k_flat(q, base_k, k):
+    """TOP_K branch on a flat index -- ``store.py:314-318`` (k clamped to p)."""
+    p = base_k.shape[0]
+    if p == 0:
+        return set()
+    return set(flat_top_k(q, base_k, min(k, p)))
+
+
+def retrieve_top_k_coarse(q, index: BlockIndex, k, p):
+    """TOP_K on the coarse block index -- ``store.py:305-312``."""
+    if p == 0:
+        return set()
+    want = max(1, -(-k // index.block_size))
+    out = set()
+    for lo, hi in index.top_blocks(q, min(want, index.n_blocks)):
+        out.update(range(lo, min(hi, p)))
+    return out
+
+
+def head_attention_retrieved(q, base_k, base_v, win_k, win_v, retrieved, initial=16, last=64):
+    """``_head_attention`` after retrieval -- ``store.py:268-293``: selected =
+    retrieved minus the base window ids, partial(selected) merged with
+    partial(base window + session rows), finalized."""
+    p = base_k.shape[0]
+    window_ids = window_base_ids(p, initial, last)
+    ret = np.fromiter(retrieved, dtype=np.int64, count=len(retrieved))
+    selected = np.setdiff1d(ret, window_ids)
+    part = Partial()
+    if selected.size:
+        part = partial_merge(part, partial_over(q, base_k[selected], base_v[selected]))
+    win_keys = [base_k[window_ids]] if window_ids.size else []
+    win_vals = [base_v[window_ids]] if window_ids.size else []
+    if win_k is not None and win_k.shape[0]:
+        win_keys.append(win_k)
+        win_vals.append(win_v)
+    if win_keys:
+        part = partial_merge(
+            part, partial_over(q, np.concatenate(win_keys), np.concatenate(win_vals)))
+    return partial_finalize(part), np.sort(selected), int(ret.size)
+
+
+def session_attention_topk(q, base_k, base_v, win_k, win_v, k, coarse=False, block_size=128,
+                           reps=4, initial=16, last=64, indexes=None):
+    """``Session.attention`` on a TOP_K plan for one layer (``store.py:191-216``
+    with ``_retrieve`` ``:305-318``). ``indexes[h]`` may hold prebuilt
+    BlockIndexes (built over the full context, as at import, ``store.py:506-509``).
+    Returns ``(out, [selected per q head], [retrieved per q head])``."""
+    q = np.atleast_2d(np.asarray(q, dtype=F32))
+    hq, d = q.shape
+    hkv = base_k.shape[0]
+    g = hq // hkv
+    p = base_k.shape[1]
+    out = np.empty((hq, d), dtype=F32)
+    sels, counts = [], []
+    for qh in range(hq):
+        h = qh // g
+        if coarse:
+            idx = indexes[h] if indexes is not None else build_block_index(base_k[h], block_size, reps)
+            ret = retrieve_top_k_coarse(q[qh], idx, k, p)
+        else:
+            ret = retrieve_top_k_flat(q[qh], base_k[h], k)
+        o, sel, cnt = head_attention_retrieved(
+            q[qh], base_k[h], base_v[h], None if win_k is None else win_k[h],
+            None if win_v is None else win_v[h], ret, initial, last)
+        out[qh] = o
+        sels.append(sel)
+        counts.append(cnt)
+    return out, sels, counts
+
+
 def block_box_bounds(keys: np.ndarray, block_size: int):
     """Per-block per-dim (min, max) boxes over contiguous blocks.
 

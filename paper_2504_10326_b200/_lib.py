@@ -36,7 +36,8 @@ EXPORTS = (
     "alaya_last_error", "alaya_version", "alaya_workspace_bytes", "alaya_dipr_attention",
     "alaya_scan", "alaya_attend", "alaya_merge_partials", "alaya_merge_states", "alaya_selected",
     "alaya_ws_status", "alaya_window_append", "alaya_block_bounds", "alaya_ws_block_stats",
-    "alaya_ws_candidate_counts",
+    "alaya_ws_candidate_counts", "alaya_topk", "alaya_block_reps", "alaya_block_topk",
+    "alaya_sparse_attention",
 )
 
 
@@ -62,6 +63,15 @@ class AlayaParams(ctypes.Structure):
         ("win_initial", ctypes.c_int32), ("win_last", ctypes.c_int32),
         ("chunk", ctypes.c_int32), ("scan_kind", ctypes.c_int32),
         ("block_filter", ctypes.c_int32),
+    ]
+
+
+class AlayaBlockIndex(ctypes.Structure):
+    """``alaya_block_index`` (include/alaya.h)."""
+
+    _fields_ = [
+        ("reps", ctypes.c_void_p), ("head_stride", ctypes.c_int64),
+        ("n_tokens", ctypes.c_int64), ("n_blocks", ctypes.c_int32), ("r", ctypes.c_int32),
     ]
 
 
@@ -109,6 +119,16 @@ def load() -> ctypes.CDLL:
     lib.alaya_ws_candidate_counts.argtypes = [P, S, i32, vp]
     lib.alaya_ws_block_stats.restype = vp
     lib.alaya_ws_block_stats.argtypes = [P, S, i32, vp]
+    i64 = ctypes.c_int64
+    lib.alaya_topk.restype = i32
+    lib.alaya_topk.argtypes = [P, S, i32, vp, i32, vp, vp, i64, vp, vp, sz, vp]
+    lib.alaya_block_reps.restype = i32
+    lib.alaya_block_reps.argtypes = [vp, i32, i32, i64, i32, i32, i32, i32, vp, i64, vp]
+    lib.alaya_block_topk.restype = i32
+    lib.alaya_block_topk.argtypes = [P, S, ctypes.POINTER(AlayaBlockIndex), i32, i32, i32, vp, vp,
+                                     i64, vp, vp, vp, vp]
+    lib.alaya_sparse_attention.restype = i32
+    lib.alaya_sparse_attention.argtypes = [P, S, i32, vp, vp, i64, vp, vp, vp, vp, vp]
     lib.alaya_ws_status.restype = vp
     lib.alaya_ws_status.argtypes = [vp]
     _lib = lib

@@ -1,5 +1,6 @@
 // C-ABI entry points (include/alaya.h): validation, workspace layout, kernel
 // dispatch over (dtype, dim, group size) and launch.
+#include <cmath>
 #include <cstdarg>
 #include <cstdlib>
 #include <cstdio>
@@ -392,6 +393,80 @@ int alaya_selected(const alaya_params* p, const alaya_seq* seqs, int batch, int6
   selected_kernel<<<batch * c.bt.Hq, kThreads, 0, c.stream>>>(c.bt, c.ws, d_ids, cap, d_selected,
                                                               d_retrieved);
   return cuda_check("selected_kernel");
+}
+
+int alaya_topk(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q, int k,
+               int64_t* d_ids, float* d_scores, int64_t cap, int32_t* d_count, void* d_ws,
+               size_t ws_bytes, void* stream) {
+  if (!p) return fail(ALAYA_ERR_ARG, "null params");
+  alaya_params pp = *p;  // every base token is a candidate: the scan with beta = inf
+  pp.beta = INFINITY;
+  pp.block_filter = 0;
+  Call c;
+  int rc = prepare(&pp, seqs, batch, d_ws, ws_bytes, stream, &c);
+  if (rc) return rc;
+  if (!d_q || !d_ids || !d_count) return fail(ALAYA_ERR_ARG, "null q/ids/count");
+  if (k < 1) return fail(ALAYA_ERR_ARG, "k must be >= 1, got %d", k);
+  if (cap < k) return fail(ALAYA_ERR_ARG, "cap %lld < k %d", (long long)cap, k);
+  for (int b = 0; b < batch; ++b)
+    if (seqs[b].token_offset != 0 || seqs[b].prefix_len != seqs[b].n)
+      return fail(ALAYA_ERR_UNSUPPORTED, "top-k runs on unsharded sequences");
+  if ((rc = run_scan(c, d_q))) return rc;
+  return launch_topk_select(c.bt, c.ws, k, d_ids, d_scores, cap, d_count, c.stream);
+}
+
+int alaya_block_reps(const void* d_k, int dtype, int n_heads, int64_t head_stride, int n, int dim,
+                     int block_size, int r, void* d_reps, int64_t reps_head_stride, void* stream) {
+  if (!d_k || !d_reps || n_heads < 1 || n < 0 || !dim_ok(dim) || block_size < 1 || r < 1)
+    return fail(ALAYA_ERR_ARG, "bad block reps arguments");
+  if (dtype != ALAYA_F32 && dtype != ALAYA_BF16) return fail(ALAYA_ERR_ARG, "bad dtype");
+  if (block_size > 16384) return fail(ALAYA_ERR_UNSUPPORTED, "block_size %d > 16384", block_size);
+  const int64_t nb = (n + block_size - 1) / block_size;
+  if (head_stride < (int64_t)n * dim || reps_head_stride < nb * r * dim)
+    return fail(ALAYA_ERR_SHAPE, "block reps: strides too small");
+  if (n == 0) return ALAYA_OK;
+  return launch_block_reps(d_k, dtype, n_heads, head_stride, n, dim, block_size, r, d_reps,
+                           reps_head_stride, static_cast<cudaStream_t>(stream));
+}
+
+int alaya_block_topk(const alaya_params* p, const alaya_seq* seqs, const alaya_block_index* bix,
+                     int batch, int block_size, int k_blocks, const float* d_q, int64_t* d_ids,
+                     int64_t cap, int32_t* d_count, int32_t* d_blocks, float* d_block_scores,
+                     void* stream) {
+  static thread_local Batch bt;
+  int rc = build_batch(p, seqs, batch, &bt);
+  if (rc) return rc;
+  if (!bix || !d_q || !d_ids || !d_count) return fail(ALAYA_ERR_ARG, "null block index/q/ids/count");
+  if (block_size < 1 || k_blocks < 1) return fail(ALAYA_ERR_ARG, "block_size and k_blocks must be >= 1");
+  static thread_local BixSet set;
+  int max_nb = 1;
+  for (int b = 0; b < batch; ++b) {
+    const alaya_block_index& x = bix[b];
+    if (x.n_blocks != (x.n_tokens + block_size - 1) / block_size || x.r < 1 ||
+        (x.n_blocks > 0 && !x.reps) || x.head_stride < (int64_t)x.n_blocks * x.r * p->dim)
+      return fail(ALAYA_ERR_SHAPE, "seq %d: block index does not match block_size %d", b, block_size);
+    set.b[b] = x;
+    max_nb = std::max(max_nb, x.n_blocks);
+  }
+  if (cap < (int64_t)k_blocks * block_size && cap < max_nb * (int64_t)block_size)
+    return fail(ALAYA_ERR_ARG, "cap %lld < k_blocks * block_size", (long long)cap);
+  return launch_block_topk(bt, p->dtype, d_q, set, max_nb, block_size, k_blocks, d_ids, cap, d_count,
+                           d_blocks, d_block_scores, static_cast<cudaStream_t>(stream));
+}
+
+int alaya_sparse_attention(const alaya_params* p, const alaya_seq* seqs, int batch,
+                           const float* d_q, const int64_t* d_ids, int64_t cap,
+                           const int32_t* d_count, float* d_out, int32_t* d_selected,
+                           int32_t* d_status, void* stream) {
+  static thread_local Batch bt;
+  int rc = build_batch(p, seqs, batch, &bt);
+  if (rc) return rc;
+  if (!d_q || !d_out || !d_count || (cap > 0 && !d_ids)) return fail(ALAYA_ERR_ARG, "null q/ids/count/out");
+  if (cap < 0) return fail(ALAYA_ERR_ARG, "negative cap");
+  for (int b = 0; b < batch; ++b)
+    if (seqs[b].prefix_len + seqs[b].w == 0) return fail(ALAYA_ERR_ARG, "attention on an empty session");
+  return launch_sparse_attention(bt, p->dtype, d_q, d_ids, cap, d_count, d_out, d_selected, d_status,
+                                 static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -48,6 +48,11 @@ struct Batch {
   int32_t seed;   // prep_kernel seeds the running max from sampled keys
 };
 
+// Coarse block indexes of a batch (kernel-parameter space).
+struct BixSet {
+  alaya_block_index b[ALAYA_MAX_BATCH];
+};
+
 // Workspace pointers (device), carved from the caller's buffer.
 struct Ws {
   int* status;

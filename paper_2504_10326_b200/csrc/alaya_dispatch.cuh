@@ -128,6 +128,16 @@ int launch_tc_scan(const Batch& bt, const alaya_seq* seqs, const float* q, const
 int launch_tc_fused(const Batch& bt, const alaya_seq* seqs, const float* q, const Ws& ws,
                     cudaStream_t st);
 bool fused_enabled();
+int launch_topk_select(const Batch& bt, const Ws& ws, int k, int64_t* ids, float* scores, int64_t cap,
+                       int32_t* count, cudaStream_t st);
+int launch_sparse_attention(const Batch& bt, int dtype, const float* q, const int64_t* ids, int64_t cap,
+                            const int32_t* count, float* out, int32_t* nsel, int* status,
+                            cudaStream_t st);
+int launch_block_reps(const void* k, int dtype, int heads, int64_t head_stride, int n, int dim,
+                      int block_size, int r, void* reps, int64_t reps_head_stride, cudaStream_t st);
+int launch_block_topk(const Batch& bt, int dtype, const float* q, const BixSet& bix, int max_nb,
+                      int block_size, int k_blocks, int64_t* ids, int64_t cap, int32_t* count,
+                      int32_t* blocks, float* bscores, cudaStream_t st);
 ALAYA_DECLARE_PICKS(ALAYA_DECL)
 #undef ALAYA_DECL
 

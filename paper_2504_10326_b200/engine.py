@@ -23,7 +23,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import AlayaParams, AlayaSeq, check
+from ._lib import AlayaBlockIndex, AlayaParams, AlayaSeq, check
 
 _DTYPES = {torch.float32: _lib.ALAYA_F32, torch.bfloat16: _lib.ALAYA_BF16}
 
@@ -140,6 +140,7 @@ class Call:
             check(_lib.ALAYA_ERR_ARG)
         self.ws = ws if ws is not None and ws.numel() >= nbytes else _WS.get(nbytes, device)
         self.ws_bytes = self.ws.numel()
+        self._dtype = dtype
 
     @property
     def stream(self) -> int:
@@ -217,6 +218,70 @@ class Call:
                                     self.stream))
         self._q_keep = q
         return part
+
+    def topk(self, q: torch.Tensor, k: int, with_scores: bool = False):
+        """Exact flat top-k per (seq, q head) (``FlatIndex.top_k``, ``index.py:60-66``):
+        ``(ids [rows, k] int64, counts [rows] int32[, scores [rows, k] fp32])``,
+        ids unordered within a row (global token ids)."""
+        q = self._q(q)
+        rows = self.B * self.params.n_query_heads
+        ids = torch.empty(rows, k, dtype=torch.int64, device=self.device)
+        cnt = torch.empty(rows, dtype=torch.int32, device=self.device)
+        sc = torch.empty(rows, k, dtype=torch.float32, device=self.device) if with_scores else None
+        check(self.lib.alaya_topk(ctypes.byref(self.params), self.seqs, self.B, q.data_ptr(), int(k),
+                                  ids.data_ptr(), sc.data_ptr() if sc is not None else None, k,
+                                  cnt.data_ptr(), self.ws.data_ptr(), self.ws_bytes, self.stream))
+        self._q_keep = q
+        return (ids, cnt, sc) if with_scores else (ids, cnt)
+
+    def block_topk(self, q: torch.Tensor, indexes: list, block_size: int, k_blocks: int,
+                   with_blocks: bool = False):
+        """TOP_K on the coarse block index (``store.py:305-312``): token ids of the
+        best ``k_blocks`` blocks per (seq, q head), clipped to the prefix.
+        ``indexes[b]`` = ``(reps [Hkv, nb, r, d], n_tokens)`` of sequence b."""
+        q = self._q(q)
+        rows = self.B * self.params.n_query_heads
+        arr = (AlayaBlockIndex * self.B)()
+        for i, (reps, n_tok) in enumerate(indexes):
+            if reps.dtype != self._dtype or not reps.is_contiguous() or reps.dim() != 4:
+                raise ValueError("block reps must be a contiguous [Hkv, blocks, r, d] tensor")
+            arr[i].reps, arr[i].head_stride = reps.data_ptr(), reps.stride(0)
+            arr[i].n_tokens, arr[i].n_blocks, arr[i].r = int(n_tok), reps.shape[1], reps.shape[2]
+        nb_max = max(int(r.shape[1]) for r, _ in indexes)
+        cap = max(1, min(k_blocks, nb_max) * block_size)
+        ids = torch.empty(rows, cap, dtype=torch.int64, device=self.device)
+        cnt = torch.empty(rows, dtype=torch.int32, device=self.device)
+        blk = sc = None
+        if with_blocks:
+            blk = torch.full((rows, k_blocks), -1, dtype=torch.int32, device=self.device)
+            sc = torch.empty(rows, k_blocks, dtype=torch.float32, device=self.device)
+        check(self.lib.alaya_block_topk(ctypes.byref(self.params), self.seqs, arr, self.B,
+                                        int(block_size), int(k_blocks), q.data_ptr(), ids.data_ptr(),
+                                        cap, cnt.data_ptr(),
+                                        blk.data_ptr() if blk is not None else None,
+                                        sc.data_ptr() if sc is not None else None, self.stream))
+        self._q_keep = q
+        return (ids, cnt, blk, sc) if with_blocks else (ids, cnt)
+
+    def sparse_attention(self, q: torch.Tensor, ids: torch.Tensor, counts: torch.Tensor,
+                         out: torch.Tensor | None = None):
+        """Attention over explicit base ids minus the window ids, merged with the
+        window partial (``store.py:268-293``) -> ``(out [B, Hq, d], selected counts)``."""
+        q = self._q(q)
+        if out is None:
+            out = torch.empty_like(q)
+        rows = self.B * self.params.n_query_heads
+        if ids.dtype != torch.int64 or ids.dim() != 2 or ids.shape[0] != rows or not ids.is_contiguous():
+            raise ValueError(f"ids must be a contiguous int64 [{rows}, cap] tensor")
+        nsel = torch.empty(rows, dtype=torch.int32, device=self.device)
+        status = self.ws[:4].view(torch.int32)
+        status.zero_()
+        check(self.lib.alaya_sparse_attention(ctypes.byref(self.params), self.seqs, self.B,
+                                              q.data_ptr(), ids.data_ptr(), ids.shape[1],
+                                              counts.data_ptr(), out.data_ptr(), nsel.data_ptr(),
+                                              status.data_ptr(), self.stream))
+        self._q_keep = q
+        return out, nsel
 
     def selected(self, cap: int):
         """Per (seq, q head) selected ids (ascending, global) + counts; after attend/attention."""
@@ -297,4 +362,25 @@ def block_bounds(k: torch.Tensor) -> torch.Tensor:
     check(lib.alaya_block_bounds(k.data_ptr(), _DTYPES[k.dtype], hkv, k.stride(0), n, d,
                                  out.data_ptr(), out.stride(0),
                                  torch.cuda.current_stream(k.device).cuda_stream))
+    return out
+
+
+def block_reps(k: torch.Tensor, block_size: int, r: int) -> torch.Tensor:
+    """BlockIndex representatives of a ``[Hkv, n, d]`` key slab (``index.py:217-243``):
+    ``[Hkv, ceil(n/block_size), r, d]`` in the key dtype, per block the r keys of
+    largest L2 norm (ties by position; a short block repeats its first)."""
+    require_cuda()
+    lib = _lib.load()
+    if k.dtype not in _DTYPES:
+        raise ValueError(f"unsupported KV dtype {k.dtype}")
+    if k.dim() != 3 or k.stride(2) != 1 or k.stride(1) != k.shape[2]:
+        raise ValueError("keys must be [heads, rows, d] with unit row stride")
+    if block_size < 1 or r < 1:
+        raise ValueError("block_size and r must be positive")
+    hkv, n, d = k.shape
+    nb = (n + block_size - 1) // block_size
+    out = torch.empty(hkv, nb, r, d, dtype=k.dtype, device=k.device)
+    check(lib.alaya_block_reps(k.data_ptr(), _DTYPES[k.dtype], hkv, k.stride(0), n, d, block_size,
+                               r, out.data_ptr(), out.stride(0),
+                               torch.cuda.current_stream(k.device).cuda_stream))
     return out

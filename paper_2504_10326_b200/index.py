@@ -1,9 +1,11 @@
-"""Flat index (reference ``sparsekv/index.py:42-70``) over device-resident keys.
+"""Flat and coarse indexes (reference ``sparsekv/index.py``) over device-resident keys.
 
 The reference's ``FlatIndex`` keeps an fp64 copy of K (``index.py:48-50``);
 here the keys stay in HBM in their storage dtype and the scan kernel
-accumulates in fp32. Graph construction and the coarse ``BlockIndex``
-heuristic are out of scope.
+accumulates in fp32. ``BlockIndex`` (``index.py:195-243``) holds the
+representatives as one device tensor ``[blocks, r, d]`` built by
+``alaya_block_reps``; ``top_blocks`` runs ``alaya_block_topk``.
+Graph construction is out of scope.
 """
 
 from __future__ import annotations
@@ -12,20 +14,114 @@ import numpy as np
 import torch
 
 from . import dipr as _dipr
+from . import engine
+
+
+def _device_keys(keys, device) -> torch.Tensor:
+    if isinstance(keys, torch.Tensor):
+        t = keys.to(device)
+        if t.dtype not in (torch.float32, torch.bfloat16):
+            t = t.float()
+        return t.contiguous()
+    return torch.from_numpy(np.ascontiguousarray(np.atleast_2d(keys), dtype=np.float32)).to(device)
+
+
+def _q_tensor(q, d, device) -> torch.Tensor:
+    qt = q if isinstance(q, torch.Tensor) else torch.from_numpy(np.asarray(q, dtype=np.float32))
+    return qt.to(device=device, dtype=torch.float32).reshape(1, 1, d)
 
 
 class FlatIndex:
     """Dense key array scanned exhaustively; token ids are 0..n-1."""
 
     def __init__(self, keys, device=None):
-        k = keys if isinstance(keys, torch.Tensor) else torch.from_numpy(
-            np.ascontiguousarray(np.atleast_2d(keys), dtype=np.float32))
-        self.keys = k.to(device or "cuda").contiguous()
+        engine.require_cuda()
+        self.keys = _device_keys(keys, torch.device(device or "cuda"))
 
     @property
     def n(self) -> int:
         return self.keys.shape[0]
 
+    def top_k(self, q, k: int) -> list[int]:
+        """Exact top-k ids by inner product, descending, ties by smaller id
+        (``index.py:60-66``). Selection on the GPU (``alaya_topk``); the k
+        results are ordered on the host by (-score, id)."""
+        if not 1 <= k <= self.n:
+            raise ValueError(f"k must be in [1, {self.n}], got {k}")
+        d = self.keys.shape[1]
+        dev = self.keys.device
+        params = engine.make_params(1, 1, d, self.keys.dtype, 0.0, 0, 0)
+        seq = engine.SeqView(k=self.keys.unsqueeze(0), v=self.keys.unsqueeze(0), n=self.n)
+        call = engine.Call([seq], params, self.keys.dtype, dev)
+        ids, cnt, sc = call.topk(_q_tensor(q, d, dev), k, with_scores=True)
+        c = int(cnt[0].item())
+        ids, sc = ids[0, :c].cpu().numpy(), sc[0, :c].cpu().numpy()
+        order = np.lexsort((ids, -sc.astype(np.float64)))
+        return ids[order].tolist()
+
     def dipr(self, q, beta: float) -> set[int]:
         """Exact DIPR result (``index.py:68-70``)."""
         return _dipr.dipr_bruteforce(q, self.keys, beta)
+
+
+class BlockIndex:
+    """Coarse index: contiguous token blocks scored by representative vectors
+    (``index.py:195-214``). ``reps`` is a device tensor ``[blocks, r, d]``."""
+
+    def __init__(self, block_size: int, n: int, reps: torch.Tensor):
+        self.block_size = int(block_size)
+        self.n_tokens = int(n)
+        self.reps_tensor = reps
+        self.starts = np.arange(0, n, block_size, dtype=np.int64)
+        self.ends = np.minimum(self.starts + block_size, n)
+
+    @property
+    def n_blocks(self) -> int:
+        return int(self.starts.shape[0])
+
+    @property
+    def reps(self) -> list[np.ndarray]:
+        """Per-block representatives as the reference lists them (min(r, len) rows)."""
+        r = self.reps_tensor.float().cpu().numpy()
+        return [r[i, : min(r.shape[1], int(e - s))] for i, (s, e) in
+                enumerate(zip(self.starts, self.ends))]
+
+    def top_blocks(self, q, k_blocks: int) -> list[tuple[int, int]]:
+        """Best ``k_blocks`` token ranges by max representative inner product,
+        ties by smaller start (``index.py:206-214``)."""
+        if not 1 <= k_blocks <= self.n_blocks:
+            raise ValueError(f"k_blocks must be in [1, {self.n_blocks}], got {k_blocks}")
+        reps = self.reps_tensor
+        d = reps.shape[-1]
+        dev = reps.device
+        params = engine.make_params(1, 1, d, reps.dtype, 0.0, 0, 0)
+        # the sequence view only carries the prefix length (no K rows are read)
+        seq = engine.SeqView(k=None, v=None, n=0, prefix_len=self.n_tokens)
+        call = engine.Call([seq], params, reps.dtype, dev)
+        _, _, blk, sc = call.block_topk(_q_tensor(q, d, dev), [(reps.unsqueeze(0), self.n_tokens)],
+                                        self.block_size, k_blocks, with_blocks=True)
+        blk, sc = blk[0].cpu().numpy(), sc[0].cpu().numpy()
+        keep = blk >= 0
+        blk, sc = blk[keep], sc[keep]
+        order = np.lexsort((blk, -sc.astype(np.float64)))
+        return [(int(self.starts[i]), int(self.ends[i])) for i in blk[order]]
+
+
+def select_representatives(block_keys, r: int) -> np.ndarray:
+    """The r keys with the largest L2 norms, ties by position (``index.py:217-228``)."""
+    bk = _device_keys(block_keys, torch.device("cuda"))
+    if not 1 <= r <= bk.shape[0]:
+        raise ValueError(f"r must be in [1, {bk.shape[0]}], got {r}")
+    reps = engine.block_reps(bk.unsqueeze(0), bk.shape[0], r)
+    return reps[0, 0].cpu().numpy()
+
+
+def build_block_index(keys, block_size: int, r: int) -> BlockIndex:
+    """Partition 0..n-1 into contiguous blocks and pick representatives
+    (``index.py:231-243``) on the GPU."""
+    if block_size < 1:
+        raise ValueError("block_size must be positive")
+    k = _device_keys(keys, torch.device("cuda"))
+    n = k.shape[0]
+    reps = engine.block_reps(k.unsqueeze(0), block_size, r)[0]
+    return BlockIndex(block_size, n, reps)

@@ -8,8 +8,11 @@ materialization: the base context is never written, ``store.py:160-189``).
 (the reference loops heads in Python, ``store.py:209``);
 ``attention_batch`` does the same for many sessions at once.
 
-Out of scope (host lifecycle, not the decode step): AVDB persistence
-(``root=``), graph/coarse index construction, TOP_K plans.
+TOP_K plans run exact flat top-k (``alaya_topk``) or the coarse block index
+(``alaya_block_topk``, representatives built at import for COARSE layers),
+then ``alaya_sparse_attention`` over the retrieved ids. FINE (graph) layers
+execute the exact flat scan (recall 1.0 >= the graph's); graph construction
+and AVDB persistence (``root=``) are out of scope.
 """
 
 from __future__ import annotations
@@ -62,6 +65,7 @@ class ContextRecord:
     plans: dict[int, Plan]
     indexes: dict = field(default_factory=dict)
     bounds: torch.Tensor | None = None  # [L, Hkv, blocks, 2, d] coarse block index (block filter)
+    block_reps: dict = field(default_factory=dict)  # layer -> [Hkv, blocks, r, d] (BlockIndex)
 
     @property
     def length(self) -> int:
@@ -224,15 +228,19 @@ class Session:
             s._check_layer(layer)
             if s.total_len == 0:
                 raise ValueError("attention on an empty session")
-            active = s.active_plan(layer)
-            beta, wi, wl = s._exec_params(active)
-            groups.setdefault((beta, wi, wl), []).append(i)
+            groups.setdefault(s._exec_key(s.active_plan(layer), layer), []).append(i)
         qd = qt.to(device=st.device, dtype=torch.float32, non_blocking=True)
         if out is None:
             out = torch.empty(len(sessions), shape.n_query_heads, shape.dim, dtype=torch.float32,
                               device=st.device)
         calls = []
-        for (beta, wi, wl), idx in groups.items():
+        for key, idx in groups.items():
+            if key[0] == "topk":
+                for c0 in range(0, len(idx), _lib.MAX_BATCH):
+                    part = idx[c0:c0 + _lib.MAX_BATCH]
+                    Session._topk_group([sessions[i] for i in part], part, key, layer, qd, out)
+                continue
+            _, beta, wi, wl = key
             for c0 in range(0, len(idx), _lib.MAX_BATCH):
                 part = idx[c0:c0 + _lib.MAX_BATCH]
                 call = st._call_for([sessions[i] for i in part], layer, beta, wi, wl)
@@ -259,12 +267,51 @@ class Session:
             return res
         return out
 
+    @staticmethod
+    def _topk_group(sessions: list["Session"], rows: list[int], key: tuple, layer: int,
+                    qd: torch.Tensor, out: torch.Tensor) -> None:
+        """TOP_K plans (``store.py:305-318``) for sessions sharing (k, mode):
+        flat exact top-k or coarse block top-k, then sparse attention over the
+        retrieved ids (``store.py:268-293``)."""
+        _, k, coarse, wi, wl = key
+        st = sessions[0]._store
+        call = st._call_for(sessions, layer, 0.0, wi, wl)
+        full = len(rows) == out.shape[0]
+        sel = None if full else torch.tensor(rows, device=st.device)
+        qs = qd if full else qd.index_select(0, sel)
+        if coarse:
+            bs = st.config.block_size
+            want = max(1, -(-k // bs))  # store.py:307
+            idxs = [(s.base.block_reps[layer], s.base.length) for s in sessions]
+            ids, cnt = call.block_topk(qs, idxs, bs, want)
+        else:
+            ids, cnt = call.topk(qs, k)  # k clamped to each prefix in the kernel (store.py:315)
+        o, _ = call.sparse_attention(qs, ids, cnt, out=out if full else None)
+        if not full:
+            out.index_copy_(0, sel, o)
+        hq = st.shape.n_query_heads
+        for j, s in enumerate(sessions):
+            r = slice(j * hq, (j + 1) * hq)
+            p = s.reused_prefix_len if s.base is not None else 0
+            s._diag = ("topk", layer, s.active_plan(layer), ids[r], cnt[r], p, wi, wl)
+
     @property
     def last_diagnostics(self) -> dict:
         """``{layer, plan, heads[{query_head, selected_base, window_base, retrieved}]}``
         (``store.py:213-215,288-292``), materialised on access."""
         if self._diag is None:
             return {}
+        if self._diag[0] == "topk":  # retrieved = the TOP_K set; selected = minus window
+            _, layer, active, ids, cnt, p, wi, wl = self._diag
+            ids, cnt = ids.cpu().numpy(), cnt.cpu().numpy()
+            window = WindowConfig(wi, wl).base_ids(p)
+            heads = []
+            for qh in range(ids.shape[0]):
+                got = ids[qh, : cnt[qh]]
+                heads.append({"selected_base": np.setdiff1d(got, window).tolist(),
+                              "window_base": window.tolist(), "retrieved": int(cnt[qh]),
+                              "query_head": qh})
+            return {"layer": layer, "plan": active, "heads": heads}
         layer, active, ids, nsel, nret, p, wi, wl = self._diag
         ids, nsel, nret = ids.cpu().numpy(), nsel.cpu().numpy(), nret.cpu().numpy()
         window = WindowConfig(wi, wl).base_ids(p).tolist()
@@ -302,15 +349,20 @@ class Session:
             k=self.base.keys[layer] if p else None, v=self.base.values[layer] if p else None, n=p,
             wk=self._wk[layer] if w else None, wv=self._wv[layer] if w else None, w=w, bounds=bnd)
 
-    def _exec_params(self, active: Plan):
-        """(beta, window initial, window last) the kernels run for a plan."""
+    def _exec_key(self, active: Plan, layer: int) -> tuple:
+        """Kernel path for a plan: ``("dipr", beta, wi, wl)`` (DIPR, FILTERED_DIPR
+        over the flat scan, FULL_ATTENTION as beta = inf without a window split)
+        or ``("topk", k, coarse, wi, wl)`` (``store.py:305-318``)."""
         cfg = self._store.config
         if active.query is QueryKind.FULL_ATTENTION:
-            return math.inf, 0, 0  # every base token selected, no window split
+            return ("dipr", math.inf, 0, 0)  # every base token selected, no window split
         if active.query is QueryKind.TOP_K:
-            raise NotImplementedError("TOP_K / coarse plans are not implemented on the B200 engine")
+            k = int(active.k or cfg.top_k)
+            coarse = (self.base is not None and layer in self.base.block_reps
+                      and self.reused_prefix_len > 0)
+            return ("topk", k, bool(coarse), cfg.window_initial, cfg.window_last)
         beta = active.beta if active.beta is not None else cfg.beta
-        return float(beta), cfg.window_initial, cfg.window_last
+        return ("dipr", float(beta), cfg.window_initial, cfg.window_last)
 
     def active_plan(self, layer: int) -> Plan:
         """Override (global or per layer) else planned (``store.py:231-250``)."""
@@ -365,8 +417,7 @@ class ContextStore:
         if not (torch.isfinite(kd).all() and torch.isfinite(vd).all()):
             raise ValueError("matrix contains non-finite elements")
         record = ContextRecord(cid, token_ids, kd, vd, self.shape, self._plans_for(n))
-        record.indexes = {(l, h): IndexKind.FLAT for l in range(self.shape.n_layers)
-                          for h in range(self.shape.n_kv_heads)}
+        self._build_indexes(record)
         record.check_invariants()
         self.contexts[cid] = record
         return cid
@@ -385,6 +436,20 @@ class ContextStore:
 
     def get(self, context_id: str) -> ContextRecord:
         return self.contexts[context_id]
+
+    def _build_indexes(self, record: ContextRecord) -> None:
+        """Per (layer, kv head) index kinds from the plans (``store.py:497-521``):
+        COARSE layers get BlockIndex representatives on the device
+        (``build_block_index``, ``index.py:231-243``); FLAT and FINE layers
+        scan the keys directly."""
+        cfg = self.config
+        record.indexes = {}
+        for layer, lp in record.plans.items():
+            for h in range(self.shape.n_kv_heads):
+                record.indexes[(layer, h)] = lp.index
+            if lp.index is IndexKind.COARSE and record.length:
+                record.block_reps[layer] = engine.block_reps(record.keys[layer], cfg.block_size,
+                                                             cfg.representatives)
 
     def _bounds_for(self, record: ContextRecord) -> torch.Tensor:
         """Coarse block index of a context, built on first use (``index.py:231-243``

@@ -90,6 +90,97 @@ def flat_session_case(name, n_layers, hq, hkv, d, n, steps, seed, beta, win_init
     print(name, "out", rec["out"].shape, "sel", rec["sel"].size)
 
 
+def topk_session_case(name, mode, k, n_layers, hq, hkv, d, n, steps, seed, win_init, win_last,
+                      clusters=16, block_size=128, reps=4, store_inputs=False):
+    """Drive the reference session API on a TOP_K plan and record it: mode
+    "flat" = Plan(TOP_K, FLAT, k) over the FlatIndex (store.py:314-318), mode
+    "coarse" = the planner's TOP_K/COARSE plan from a large memory budget
+    (planner.py:113-115) over BlockIndex(block_size, reps) (store.py:305-312)."""
+    from sparsekv.planner import IndexKind, Plan, QueryKind
+    shape = ModelShape(n_layers, hq, hkv, d)
+    common = dict(window_initial=win_init, window_last=win_last, short_context_threshold=0,
+                  first_layers=tuple(range(n_layers)), top_k=k)
+    if mode == "coarse":
+        cfg = EngineConfig(memory_budget_bytes=10**12, block_size=block_size,
+                           representatives=reps, **common)
+    else:
+        cfg = EngineConfig(**common)
+    spec = WorkloadSpec(n_tokens=n, shape=shape, seed=seed, clusters=clusters)
+    ctx = make_context(spec)
+    keys, values = ctx.keys, ctx.values
+    gen_hash = sha(ctx.token_ids, keys, values, ctx.centers)
+    tids, qs, ks, vs = decode_step_inputs(spec, steps, ctx.centers)
+    step_hash = sha(tids, qs, ks, vs)
+    db = ContextStore(shape, cfg)
+    db.import_context(ctx.token_ids, keys, values)
+    session, _ = db.create_session(ctx.token_ids)
+    if mode == "flat":
+        session.plan_override = Plan(QueryKind.TOP_K, IndexKind.FLAT, k=k)
+    rec = {"shape": np.array([n_layers, hq, hkv, d, n, steps, seed, clusters]),
+           "beta": np.float64(0.0), "window": np.array([win_init, win_last]),
+           "bf16": np.int64(0), "layers": np.arange(n_layers),
+           "topk": np.array([k, block_size, reps, 1 if mode == "coarse" else 0])}
+    outs, sel_flat, sel_off, retrieved = [], [], [0], []
+    for step in range(steps):
+        for layer in range(n_layers):
+            session.update(qs[step, layer], ks[step, layer], vs[step, layer], layer)
+        session.record_token(int(tids[step]))
+        for layer in range(n_layers):
+            plan = session.active_plan(layer)
+            assert plan.query is QueryKind.TOP_K
+            assert plan.index is (IndexKind.COARSE if mode == "coarse" else IndexKind.FLAT)
+            o = session.attention(qs[step, layer], layer)
+            outs.append(o)
+            for info in session.last_diagnostics["heads"]:
+                sel_flat.extend(info["selected_base"])
+                sel_off.append(len(sel_flat))
+                retrieved.append(info["retrieved"])
+    rec.update(out=np.stack(outs), sel=np.array(sel_flat, dtype=np.int32),
+               sel_off=np.array(sel_off, dtype=np.int64),
+               retrieved=np.array(retrieved, dtype=np.int64))
+    rec["gen_sha"] = np.array(gen_hash)
+    rec["step_sha"] = np.array(step_hash)
+    if store_inputs:
+        rec.update(keys=keys, values=values, q=qs, k=ks, v=vs)
+    np.savez_compressed(OUT / f"{name}.npz", **rec)
+    print(name, "out", rec["out"].shape, "sel", rec["sel"].size)
+
+
+def topk_known_answers():
+    """FlatIndex.top_k / BlockIndex.top_blocks vectors from the real reference."""
+    from sparsekv.index import FlatIndex, build_block_index
+    rng = np.random.default_rng(4242)
+    cases = {}
+    q = rng.standard_normal(64).astype(np.float32) * 3
+    keys = rng.standard_normal((1200, 64)).astype(np.float32) * 3
+    keys[700] = keys[300]  # an exact tie: smaller id first (index.py:64-65)
+    keys[701] = keys[300]
+    cases["q"], cases["k"] = q, keys
+    ks = np.array([1, 2, 3, 10, 100, 1200])
+    cases["ks"] = ks
+    flat, off = [], [0]
+    for k in ks:
+        flat.extend(FlatIndex(keys).top_k(q, int(k)))
+        off.append(len(flat))
+    cases["topk"], cases["topk_off"] = np.array(flat, np.int64), np.array(off)
+    # tie at the cut: k such that the tied triple straddles the boundary
+    scores = keys.astype(np.float64) @ q.astype(np.float64)
+    rank = int((scores > scores[300]).sum())
+    cases["tie_k"] = np.array([rank + 1, rank + 2])
+    cases["tie_topk1"] = np.array(FlatIndex(keys).top_k(q, rank + 1))
+    cases["tie_topk2"] = np.array(FlatIndex(keys).top_k(q, rank + 2))
+    # block index: 1200 keys, blocks of 64 (last block partial: 1200 = 18*64 + 48), r = 4
+    bi = build_block_index(keys, 64, 4)
+    cases["blk_reps"] = np.concatenate([r for r in bi.reps])
+    blocks, boff = [], [0]
+    for kb in (1, 3, bi.n_blocks):
+        blocks.extend([s for s, _ in bi.top_blocks(q, kb)])
+        boff.append(len(blocks))
+    cases["blk_top"], cases["blk_off"] = np.array(blocks, np.int64), np.array(boff)
+    np.savez_compressed(OUT / "topk_known_answers.npz", **cases)
+    print("topk_known_answers")
+
+
 def known_answers():
     """Known-answer DIPR / window cases lifted from the reference's own tests."""
     rng = np.random.default_rng(12345)  # reference tests/conftest.py:7-9
@@ -124,6 +215,15 @@ def known_answers():
 
 def main():
     known_answers()
+    topk_known_answers()
+    topk_session_case("tiny_topk_flat", "flat", 20, 2, 4, 2, 16, 200, 2, seed=11, win_init=4,
+                      win_last=8, clusters=6, store_inputs=True)
+    topk_session_case("tiny_topk_coarse", "coarse", 40, 2, 4, 2, 16, 203, 2, seed=12, win_init=4,
+                      win_last=8, clusters=6, block_size=16, reps=3, store_inputs=True)
+    topk_session_case("llama_4k_topk_flat", "flat", 100, 1, 32, 8, 128, 4096, 1, seed=0,
+                      win_init=16, win_last=64)
+    topk_session_case("llama_4k_topk_coarse", "coarse", 300, 1, 32, 8, 128, 4096, 1, seed=0,
+                      win_init=16, win_last=64)
     # tiny shapes with stored inputs: edge cases of the window/selection logic
     flat_session_case("tiny_gqa", 2, 4, 2, 16, 200, 3, seed=1, beta=8.0,
                       win_init=4, win_last=8, clusters=6, store_inputs=True)

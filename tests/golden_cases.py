@@ -17,6 +17,8 @@ from oracle import alaya_oracle as O
 GOLDEN = Path(__file__).resolve().parent / "golden"
 SESSION_CASES = ["tiny_gqa", "tiny_short", "tiny_nowin", "llama_4k_fp32", "llama_4k_bf16",
                  "qwen_2k_fp32"]
+# TOP_K plans (flat FlatIndex.top_k and coarse BlockIndex.top_blocks)
+TOPK_CASES = ["tiny_topk_flat", "tiny_topk_coarse", "llama_4k_topk_flat", "llama_4k_topk_coarse"]
 
 
 def sha(*arrays) -> str:
@@ -49,6 +51,7 @@ class SessionCase:
     out: np.ndarray       # reference outputs, (steps*len(layers), Hq, d)
     sel: list             # reference selected ids per (step, layer, q head)
     retrieved: np.ndarray
+    topk: tuple | None = None  # (k, block_size, reps, coarse) for TOP_K cases
 
     def call_index(self, step: int, li: int) -> int:
         return step * len(self.layers) + li
@@ -79,7 +82,8 @@ def load_session_case(name: str) -> SessionCase:
     w = z["window"]
     return SessionCase(name, L, hq, hkv, d, n, steps, seed, float(z["beta"]), int(w[0]),
                        int(w[1]), bf16, [int(x) for x in z["layers"]], keys, values, q, k, v,
-                       z["out"], sel, z["retrieved"])
+                       z["out"], sel, z["retrieved"],
+                       tuple(int(x) for x in z["topk"]) if "topk" in z else None)
 
 
 def window_rows(case: SessionCase, step: int, layer: int):

@@ -1,0 +1,185 @@
+"""GPU parity of the TOP_K plans (flat ``FlatIndex.top_k`` and the coarse
+``BlockIndex``), through the C-ABI (alaya_topk / alaya_block_reps /
+alaya_block_topk / alaya_sparse_attention), against golden fixtures of the
+real reference and the CPU oracle.
+
+Rules: top-k sets identical except tokens whose fp64 score lies within EPS of
+the k-th score (block sets: blocks whose score lies within EPS of the cut
+block's); outputs within 1e-5 norm-relative error of the oracle evaluated on
+the GPU's own retrieved set.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import alaya_oracle as O
+from tests.golden_cases import GOLDEN, TOPK_CASES, load_session_case, window_rows
+
+pytestmark = pytest.mark.gpu
+
+EPS = 1e-4
+TOL = 1e-5
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def topk_set_ok(got, want, scores, k):
+    got, want = set(int(x) for x in got), set(int(x) for x in want)
+    if got == want:
+        return True
+    kth = np.sort(scores)[::-1][min(k, scores.size) - 1]
+    return len(got) == len(want) and all(abs(scores[t] - kth) <= EPS for t in got ^ want)
+
+
+def test_flat_topk_reference_hand_cases(cuda_ok):
+    import paper_2504_10326_b200 as P
+    pad = lambda a: np.pad(np.asarray(a, np.float32), ((0, 0), (0, 14)))  # noqa: E731
+    q = np.zeros(16, np.float32); q[0] = 1.0
+    assert P.FlatIndex(pad([[3, 0], [1, 0], [2, 0]])).top_k(q, 2) == [0, 2]
+    assert P.FlatIndex(pad([[2, 0], [2, 0], [3, 0]])).top_k(q, 3) == [2, 0, 1]
+    with pytest.raises(ValueError):
+        P.FlatIndex(pad(np.ones((4, 2)))).top_k(q, 5)
+
+
+def test_flat_topk_known_answers(cuda_ok):
+    import paper_2504_10326_b200 as P
+    z = np.load(GOLDEN / "topk_known_answers.npz")
+    idx = P.FlatIndex(z["k"])
+    scores = O.inner_products(z["k"], z["q"])
+    off = z["topk_off"]
+    for i, k in enumerate(z["ks"]):
+        want = z["topk"][off[i]:off[i + 1]].tolist()
+        got = idx.top_k(z["q"], int(k))
+        assert topk_set_ok(got, want, scores, int(k)), k
+        if set(got) == set(want):
+            assert got == want  # same order: descending score, ties by smaller id
+    # exact ties straddling the cut: the smaller ids win
+    t1, t2 = (int(x) for x in z["tie_k"])
+    assert idx.top_k(z["q"], t1) == z["tie_topk1"].tolist()
+    assert idx.top_k(z["q"], t2) == z["tie_topk2"].tolist()
+
+
+def test_flat_topk_bf16_and_large(cuda_ok, rng):
+    import torch
+
+    import paper_2504_10326_b200 as P
+    keys = O.bf16_round(rng.standard_normal((20000, 128)).astype(np.float32))
+    q = rng.standard_normal(128).astype(np.float32)
+    scores = O.inner_products(keys, q)
+    for dt in (torch.float32, torch.bfloat16):
+        idx = P.FlatIndex(torch.from_numpy(keys).to("cuda", dt))
+        for k in (1, 100, 5000, 20000):
+            got = idx.top_k(q, k)
+            assert topk_set_ok(got, O.flat_top_k(q, keys, k), scores, k), (dt, k)
+
+
+def test_block_index_known_answers(cuda_ok):
+    import paper_2504_10326_b200 as P
+    from paper_2504_10326_b200.index import build_block_index
+    z = np.load(GOLDEN / "topk_known_answers.npz")
+    bi = build_block_index(z["k"], 64, 4)
+    assert np.array_equal(np.concatenate(bi.reps), z["blk_reps"])  # fp64 norms: exact reps
+    boff = z["blk_off"]
+    for i, kb in enumerate((1, 3, bi.n_blocks)):
+        got = [s for s, _ in bi.top_blocks(z["q"], kb)]
+        assert got == z["blk_top"][boff[i]:boff[i + 1]].tolist()
+    # reference tests/test_index.py:205-224 (hand ranking, ties by smaller start)
+    pad = lambda a: np.pad(np.asarray(a, np.float32), ((0, 0), (0, 15)))  # noqa: E731
+    q = np.zeros(16, np.float32); q[0] = 1.0
+    idx = build_block_index(pad([[4.0], [1.0], [3.0], [2.0]]), 1, 1)
+    assert idx.top_blocks(q, 4) == [(0, 1), (2, 3), (3, 4), (1, 2)]
+    idx = build_block_index(pad([[2.0], [2.0], [1.0]]), 1, 1)
+    assert idx.top_blocks(q, 2) == [(0, 1), (1, 2)]
+    with pytest.raises(ValueError):
+        idx.top_blocks(q, 4)
+    assert P.FlatIndex is not None
+
+
+def make_topk_store(c):
+    import paper_2504_10326_b200 as P
+    k, bs, reps, coarse = c.topk
+    shape = P.ModelShape(c.n_layers, c.hq, c.hkv, c.d)
+    common = dict(window_initial=c.win_init, window_last=c.win_last, short_context_threshold=0,
+                  first_layers=tuple(range(c.n_layers)), top_k=k)
+    if coarse:
+        cfg = P.EngineConfig(memory_budget_bytes=10**12, block_size=bs, representatives=reps,
+                             **common)
+    else:
+        cfg = P.EngineConfig(**common)
+    return P, P.ContextStore(shape, cfg)
+
+
+@pytest.mark.parametrize("name", TOPK_CASES)
+def test_topk_session_matches_reference(cuda_ok, name):
+    c = load_session_case(name)
+    k, bs, reps, coarse = c.topk
+    P, db = make_topk_store(c)
+    tokens = np.arange(c.n, dtype=np.int64) + 3
+    db.import_context(tokens, c.keys, c.values)
+    sess, _ = db.create_session(tokens)
+    if not coarse:
+        sess.plan_override = P.Plan(P.QueryKind.TOP_K, P.IndexKind.FLAT, k=k)
+    worst = 0.0
+    bidx = [O.build_block_index(c.keys[0, h], bs, reps) for h in range(c.hkv)] if coarse else None
+    for step in range(c.steps):
+        for layer in range(c.n_layers):
+            sess.update(c.q[step, layer], c.k[step, layer], c.v[step, layer], layer)
+        for li, layer in enumerate(c.layers):
+            out = sess.attention(c.q[step, layer], layer)
+            diag = sess.last_diagnostics
+            assert diag["plan"].query is P.QueryKind.TOP_K
+            idx = c.call_index(step, li)
+            wk, wv = window_rows(c, step, layer)
+            for qh in range(c.hq):
+                h = qh // (c.hq // c.hkv)
+                q = c.q[step, layer, qh]
+                info = diag["heads"][qh]
+                want = c.selected(step, li, qh)
+                got = np.asarray(info["selected_base"], np.int64)
+                if not np.array_equal(got, want):  # only legitimate boundary flips
+                    if coarse:
+                        bi = O.build_block_index(c.keys[layer, h], bs, reps)
+                        sc = bi.block_scores(q)
+                        want_k = max(1, -(-k // bs))
+                        cut = np.sort(sc)[::-1][min(want_k, sc.size) - 1]
+                        flips = {int(t) // bs for t in set(got.tolist()) ^ set(want.tolist())}
+                        assert all(abs(sc[b] - cut) <= EPS for b in flips), (step, layer, qh)
+                    else:
+                        s = O.inner_products(c.keys[layer, h], q)
+                        assert topk_set_ok(got, want, s, min(k, c.n)), (step, layer, qh)
+                assert info["retrieved"] == c.retrieved[idx * c.hq + qh]
+                ret = set(got.tolist()) | set(O.window_base_ids(c.n, c.win_init, c.win_last).tolist())
+                o_ref, _, _ = O.head_attention_retrieved(q, c.keys[layer, h], c.values[layer, h],
+                                                         wk[h], wv[h], got, c.win_init, c.win_last)
+                e = rel(out[qh], o_ref)
+                worst = max(worst, e)
+                assert e <= TOL, (step, layer, qh, e)
+                if np.array_equal(got, want):
+                    assert rel(out[qh], c.out[idx, qh]) <= TOL
+                del ret
+    del bidx
+    print(f"{name}: worst norm-relative error {worst:.2e}")
+
+
+def test_topk_batch_mixed_plans(cuda_ok, rng):
+    """A batch mixing DIPR and TOP_K sessions of one store runs each plan's path."""
+    import paper_2504_10326_b200 as P
+    L, hq, hkv, d, n = 1, 8, 2, 64, 3000
+    keys = rng.standard_normal((L, hkv, n, d)).astype(np.float32)
+    vals = rng.standard_normal((L, hkv, n, d)).astype(np.float32)
+    cfg = P.EngineConfig(short_context_threshold=0, first_layers=(0,), beta=5.0, top_k=50)
+    db = P.ContextStore(P.ModelShape(L, hq, hkv, d), cfg)
+    tok = np.arange(n)
+    db.import_context(tok, keys, vals)
+    s1, _ = db.create_session(tok)
+    s2, _ = db.create_session(tok)
+    s2.plan_override = P.Plan(P.QueryKind.TOP_K, P.IndexKind.FLAT, k=50)
+    q = rng.standard_normal((2, hq, d)).astype(np.float32)
+    out = P.Session.attention_batch([s1, s2], q, 0)
+    o1, _, _ = O.session_attention_flat(q[0], keys[0], vals[0], None, None, 5.0)
+    o2, _, _ = O.session_attention_topk(q[1], keys[0], vals[0], None, None, 50)
+    assert rel(out[0], o1) <= TOL and rel(out[1], o2) <= TOL

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from oracle import alaya_oracle as O
-from tests.golden_cases import GOLDEN, SESSION_CASES, load_session_case, window_rows
+from tests.golden_cases import GOLDEN, SESSION_CASES, TOPK_CASES, load_session_case, window_rows
 
 
 def test_known_answer_hand_case():
@@ -82,3 +82,55 @@ def test_box_bound_is_sound(rng):
     s = O.inner_products(keys, q)
     for b in range(ub.size):
         assert s[b * 128:(b + 1) * 128].max() <= ub[b] + 1e-9
+
+
+# --------------------------------------------------------------------------
+# TOP_K plans (flat FlatIndex.top_k and the coarse BlockIndex)
+# --------------------------------------------------------------------------
+
+def test_topk_reference_hand_cases():
+    """Known answers of the reference's tests/test_index.py:33-41,205-224."""
+    q = np.array([1.0, 0.0], np.float32)
+    assert O.flat_top_k(q, np.array([[3, 0], [1, 0], [2, 0]], np.float32), 2) == [0, 2]
+    assert O.flat_top_k(q, np.array([[2, 0], [2, 0], [3, 0]], np.float32), 3) == [2, 0, 1]
+    with pytest.raises(ValueError):
+        O.flat_top_k(q, np.ones((4, 2), np.float32), 5)
+    idx = O.build_block_index(np.array([[4.0], [1.0], [3.0], [2.0]], np.float32), 1, 1)
+    assert idx.top_blocks(np.array([1.0], np.float32), 4) == [(0, 1), (2, 3), (3, 4), (1, 2)]
+    idx = O.build_block_index(np.array([[2.0], [2.0], [1.0]], np.float32), 1, 1)
+    assert idx.top_blocks(np.array([1.0], np.float32), 2) == [(0, 1), (1, 2)]
+    keys = np.array([[1, 0], [1, 0], [0, 1], [0, 1]], np.float32)
+    assert O.build_block_index(keys, 2, 1).top_blocks(q, 1) == [(0, 2)]
+
+
+def test_topk_known_answers_vs_reference():
+    z = np.load(GOLDEN / "topk_known_answers.npz")
+    off = z["topk_off"]
+    for i, k in enumerate(z["ks"]):
+        assert O.flat_top_k(z["q"], z["k"], int(k)) == z["topk"][off[i]:off[i + 1]].tolist()
+    t1, t2 = (int(x) for x in z["tie_k"])
+    assert O.flat_top_k(z["q"], z["k"], t1) == z["tie_topk1"].tolist()
+    assert O.flat_top_k(z["q"], z["k"], t2) == z["tie_topk2"].tolist()
+    bi = O.build_block_index(z["k"], 64, 4)
+    assert np.array_equal(np.concatenate(bi.reps), z["blk_reps"])
+    boff = z["blk_off"]
+    for i, kb in enumerate((1, 3, bi.n_blocks)):
+        got = [s for s, _ in bi.top_blocks(z["q"], kb)]
+        assert got == z["blk_top"][boff[i]:boff[i + 1]].tolist()
+
+
+@pytest.mark.parametrize("name", TOPK_CASES)
+def test_topk_session_bit_exact_vs_reference(name):
+    c = load_session_case(name)
+    k, bs, reps, coarse = c.topk
+    for step in range(c.steps):
+        for li, layer in enumerate(c.layers):
+            wk, wv = window_rows(c, step, layer)
+            out, sels, counts = O.session_attention_topk(
+                c.q[step, layer], c.keys[layer], c.values[layer], wk, wv, k, bool(coarse), bs,
+                reps, c.win_init, c.win_last)
+            idx = c.call_index(step, li)
+            assert np.array_equal(out, c.out[idx])
+            for qh in range(c.hq):
+                assert np.array_equal(sels[qh], c.selected(step, li, qh))
+                assert counts[qh] == c.retrieved[idx * c.hq + qh]

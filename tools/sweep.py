@@ -128,6 +128,43 @@ if "4" in which:
                       label="config4 Qwen2.5-14B shape (40/8)")
         del K, V
         torch.cuda.empty_cache()
+if "topk" in which:
+    # TOP_K plans at 128K: exact flat top-k (scan with every token a candidate +
+    # radix select) and the coarse block index (r=4 reps per 128-token block),
+    # each followed by sparse attention over the retrieved ids + window
+    from paper_2504_10326_b200 import engine as E
+    for B in (1, 4):
+        K, V, centers, g = make(B, 8, a.ctx, 128, locality=False, seed=300 + B)
+        hq, hkv, n, d = 32, 8, a.ctx, 128
+        params = E.make_params(hq, hkv, d, torch.bfloat16, 0.0, 16, 64)
+        call = E.Call([E.SeqView(k=K[b], v=V[b], n=n) for b in range(B)], params, torch.bfloat16, dev)
+        pick = torch.randint(0, 16, (B, hq), generator=g, device=dev)
+        q = (centers[pick] + 0.25 * torch.randn(B, hq, d, generator=g, device=dev)).float()
+        reps = [(E.block_reps(K[b], 128, 4), n) for b in range(B)]
+        for mode, k in (("flat", 100), ("flat", 2048), ("coarse", 100), ("coarse", 2048)):
+            def step():
+                if mode == "flat":
+                    ids, cnt = call.topk(q, k)
+                else:
+                    ids, cnt = call.block_topk(q, reps, 128, max(1, -(-k // 128)))
+                call.sparse_attention(q, ids, cnt)
+            for _ in range(3):
+                step()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(a.reps):
+                step()
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / a.reps / 1e3
+            kbytes = B * hkv * n * d * 2 if mode == "flat" else B * hkv * (n // 128) * 4 * d * 2
+            emit({"label": f"TOP_K {mode}", "B": B, "Hq": hq, "ctx": n, "k": k,
+                  "us_per_layer_call": round(t * 1e6, 1), "query_heads_per_s": round(B * hq / t),
+                  "scanned_bytes": kbytes, "scanned_GBps": round(kbytes / t / 1e9, 1),
+                  "frac_of_measured_hbm": round(kbytes / t / 1e9 / peak, 4)})
+        del K, V, call, reps
+        torch.cuda.empty_cache()
 if a.out:
     with open(a.out, "w") as fh:
         for d in lines:
