@@ -220,6 +220,43 @@ int alaya_sparse_attention(const alaya_params* p, const alaya_seq* seqs, int bat
                            const int32_t* d_count, float* d_out, int32_t* d_selected,
                            int32_t* d_status, void* stream);
 
+/* ---- AVDB vector files (reference vfs.py, docs/file-format.md) ---------- */
+
+typedef struct {
+  uint32_t dim;
+  uint32_t element_width;   /* 16 (IEEE half) or 32 */
+  uint64_t n_vectors;
+  uint32_t n_data_blocks;
+  uint32_t n_index_blocks;  /* graph adjacency blocks (not loaded here) */
+  uint32_t n_tombstones;    /* ids marked deleted (vectors still loaded, vfs.py:310-314) */
+  uint32_t pad_;
+  uint64_t file_bytes;
+  uint64_t directory_offset;
+  uint64_t index_head;
+} alaya_avdb_info;
+
+/* Header + directory chain of one file (read_header / read_directory,
+ * vfs.py:247-286). Format errors -> ALAYA_ERR_ARG naming path and offset. */
+int alaya_avdb_stat(const char* path, alaya_avdb_info* out);
+
+/* write_vector_file (vfs.py:188-244) for a vector-only file: host fp32
+ * vectors [n][dim], element_width 32 or 16 (half, round-to-nearest-even).
+ * Byte-identical to the reference writer. Host only. */
+int alaya_avdb_write(const char* path, const float* vectors, int64_t n, int dim, int element_width);
+
+/* Pinned staging bytes alaya_avdb_load needs for these files (0 on error). */
+size_t alaya_avdb_staging_bytes(const char* const* paths, int n_files);
+
+/* read_vector_file (vfs.py:289-338) of n_files files of n vectors x dim into
+ * the device slab d_dst[f*dst_file_stride + row*dim + e] (dst_dtype F32:
+ * exact widening, BF16: round to nearest even). Each file image is read into
+ * h_staging (PINNED host memory, >= alaya_avdb_staging_bytes) and one
+ * stream-ordered kernel unpacks the data blocks straight from it. h_staging
+ * must stay untouched until the stream passes this call. */
+int alaya_avdb_load(const char* const* paths, int n_files, int64_t n, int dim, int dst_dtype,
+                    void* d_dst, int64_t dst_file_stride, void* h_staging, size_t staging_bytes,
+                    void* stream);
+
 /* Blocks kept / blocks considered by the block filter in the last scan on
  * this workspace: device pointer to two int32 (valid after the scan). */
 int* alaya_ws_block_stats(const alaya_params* p, const alaya_seq* seqs, int batch, void* d_ws);

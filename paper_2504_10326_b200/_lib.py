@@ -37,7 +37,8 @@ EXPORTS = (
     "alaya_scan", "alaya_attend", "alaya_merge_partials", "alaya_merge_states", "alaya_selected",
     "alaya_ws_status", "alaya_window_append", "alaya_block_bounds", "alaya_ws_block_stats",
     "alaya_ws_candidate_counts", "alaya_topk", "alaya_block_reps", "alaya_block_topk",
-    "alaya_sparse_attention",
+    "alaya_sparse_attention", "alaya_avdb_stat", "alaya_avdb_write", "alaya_avdb_staging_bytes",
+    "alaya_avdb_load",
 )
 
 
@@ -72,6 +73,18 @@ class AlayaBlockIndex(ctypes.Structure):
     _fields_ = [
         ("reps", ctypes.c_void_p), ("head_stride", ctypes.c_int64),
         ("n_tokens", ctypes.c_int64), ("n_blocks", ctypes.c_int32), ("r", ctypes.c_int32),
+    ]
+
+
+class AlayaAvdbInfo(ctypes.Structure):
+    """``alaya_avdb_info`` (include/alaya.h)."""
+
+    _fields_ = [
+        ("dim", ctypes.c_uint32), ("element_width", ctypes.c_uint32),
+        ("n_vectors", ctypes.c_uint64), ("n_data_blocks", ctypes.c_uint32),
+        ("n_index_blocks", ctypes.c_uint32), ("n_tombstones", ctypes.c_uint32),
+        ("pad_", ctypes.c_uint32), ("file_bytes", ctypes.c_uint64),
+        ("directory_offset", ctypes.c_uint64), ("index_head", ctypes.c_uint64),
     ]
 
 
@@ -129,6 +142,15 @@ def load() -> ctypes.CDLL:
                                      i64, vp, vp, vp, vp]
     lib.alaya_sparse_attention.restype = i32
     lib.alaya_sparse_attention.argtypes = [P, S, i32, vp, vp, i64, vp, vp, vp, vp, vp]
+    cp, cpp = ctypes.c_char_p, ctypes.POINTER(ctypes.c_char_p)
+    lib.alaya_avdb_stat.restype = i32
+    lib.alaya_avdb_stat.argtypes = [cp, ctypes.POINTER(AlayaAvdbInfo)]
+    lib.alaya_avdb_write.restype = i32
+    lib.alaya_avdb_write.argtypes = [cp, vp, i64, i32, i32]
+    lib.alaya_avdb_staging_bytes.restype = sz
+    lib.alaya_avdb_staging_bytes.argtypes = [cpp, i32]
+    lib.alaya_avdb_load.restype = i32
+    lib.alaya_avdb_load.argtypes = [cpp, i32, i64, i32, i32, vp, i64, vp, sz, vp]
     lib.alaya_ws_status.restype = vp
     lib.alaya_ws_status.argtypes = [vp]
     _lib = lib

@@ -12,19 +12,22 @@ TOP_K plans run exact flat top-k (``alaya_topk``) or the coarse block index
 (``alaya_block_topk``, representatives built at import for COARSE layers),
 then ``alaya_sparse_attention`` over the retrieved ids. FINE (graph) layers
 execute the exact flat scan (recall 1.0 >= the graph's); graph construction
-and AVDB persistence (``root=``) are out of scope.
+is out of scope. ``root=`` persists contexts as the
+reference's AVDB files and reloads them pinned host -> HBM (``vfs.py``).
 """
 
 from __future__ import annotations
 
 import hashlib
+import json
 import math
 from dataclasses import dataclass, field
+from pathlib import Path
 
 import numpy as np
 import torch
 
-from . import _lib, engine
+from . import _lib, engine, vfs
 from .config import EngineConfig
 from .core import ModelShape, WindowConfig
 from .planner import IndexKind, Plan, PlanRequest, QueryKind, plan as make_plan
@@ -391,8 +394,9 @@ class ContextStore:
 
     def __init__(self, shape: ModelShape, config: EngineConfig | None = None, root=None,
                  pool=None, device=None, log_queries: bool = True):
-        if root is not None or pool is not None:
-            raise NotImplementedError("AVDB persistence / buffer pool are out of scope")
+        if pool is not None:
+            raise NotImplementedError("the block buffer pool is out of scope: AVDB files load "
+                                      "through pinned host memory straight into HBM")
         engine.require_cuda()
         self.shape = shape
         self.config = config or EngineConfig()
@@ -401,6 +405,11 @@ class ContextStore:
         self.log_queries = log_queries
         self.contexts: dict[str, ContextRecord] = {}
         self._calls: dict = {}
+        self.root = Path(root) if root is not None else None
+        self.pool = None
+        if self.root is not None:
+            self.root.mkdir(parents=True, exist_ok=True)
+            self._load_existing()
 
     def import_context(self, token_ids, keys, values, queries=None) -> str:
         """Import K/V ``[L, Hkv, n, d]`` (numpy or torch) to the device (``store.py:388-422``)."""
@@ -420,6 +429,8 @@ class ContextStore:
         self._build_indexes(record)
         record.check_invariants()
         self.contexts[cid] = record
+        if self.root is not None:
+            self._persist(record)
         return cid
 
     def create_session(self, token_ids):
@@ -436,6 +447,93 @@ class ContextStore:
 
     def get(self, context_id: str) -> ContextRecord:
         return self.contexts[context_id]
+
+    def store(self, session: Session) -> str:
+        """Materialize a session (base prefix + window) into a new context
+        (``store.py:440-477``); the concatenation stays on the device."""
+        p = session.reused_prefix_len
+        if session.total_len == 0:
+            raise ValueError("cannot store an empty session")
+        shape = self.shape
+        base_tokens = (session.base.token_ids[:p] if session.base is not None
+                       else np.empty(0, dtype=np.int64))
+        token_ids = np.concatenate([base_tokens,
+                                    np.asarray(session.generated_token_ids, dtype=np.int64)])
+        if token_ids.shape[0] != session.total_len:
+            raise ValueError(f"recorded token ids ({token_ids.shape[0]}) do not cover the "
+                             f"session length ({session.total_len}); call record_token per step")
+        n = session.total_len
+        w = session.window_len
+        if any(wl != w for wl in session._wlen):
+            raise ValueError("every layer's window must hold the same number of rows to store")
+        keys = torch.empty(shape.n_layers, shape.n_kv_heads, n, shape.dim, dtype=self.kv_dtype,
+                           device=self.device)
+        values = torch.empty_like(keys)
+        if p and session.base is not None:
+            keys[:, :, :p] = session.base.keys[:, :, :p]
+            values[:, :, :p] = session.base.values[:, :, :p]
+        if w:
+            keys[:, :, p:] = session._wk[:, :, :w]
+            values[:, :, p:] = session._wv[:, :, :w]
+        return self.import_context(token_ids, keys, values)
+
+    # -- persistence (AVDB files, reference store.py:523-609) ------------------
+    def context_dir(self, context_id: str) -> Path:
+        if self.root is None:
+            raise ValueError("store has no persistence root")
+        return self.root / "contexts" / context_id
+
+    def _persist(self, record: ContextRecord) -> None:
+        """meta.json + tokens.bin + one AVDB file per (layer, kv head) for K and
+        V (``store.py:527-565``), written by the native writer."""
+        out = self.context_dir(record.context_id)
+        out.mkdir(parents=True, exist_ok=True)
+        (out / "tokens.bin").write_bytes(record.token_ids.tobytes())
+        meta = {
+            "context_id": record.context_id,
+            "n_tokens": record.length,
+            "shape": {"n_layers": self.shape.n_layers, "n_query_heads": self.shape.n_query_heads,
+                      "n_kv_heads": self.shape.n_kv_heads, "dim": self.shape.dim},
+            "element_width": self.config.element_width,
+            "plans": {str(layer): {"query": p.query.value, "index": p.index.value}
+                      for layer, p in record.plans.items()},
+        }
+        (out / "meta.json").write_text(json.dumps(meta, indent=2, sort_keys=True) + "\n")
+        for layer in range(self.shape.n_layers):
+            kh = record.keys[layer].float().cpu().numpy()
+            vh = record.values[layer].float().cpu().numpy()
+            for head in range(self.shape.n_kv_heads):
+                vfs.write_vector_file(out / f"L{layer}H{head}.k.avdb", kh[head],
+                                      element_width=self.config.element_width)
+                vfs.write_vector_file(out / f"L{layer}H{head}.v.avdb", vh[head],
+                                      element_width=self.config.element_width)
+
+    def _load_existing(self) -> None:
+        """Reopen persisted contexts (``store.py:567-609``): every layer's K and V
+        files go pinned host -> HBM through ``alaya_avdb_load``."""
+        base = self.root / "contexts"
+        if not base.exists():
+            return
+        sh = self.shape
+        for ctx_dir in sorted(base.iterdir()):
+            meta_path = ctx_dir / "meta.json"
+            if not meta_path.exists():
+                continue
+            meta = json.loads(meta_path.read_text())
+            token_ids = np.frombuffer((ctx_dir / "tokens.bin").read_bytes(), dtype=np.int64).copy()
+            n = int(meta["n_tokens"])
+            keys = torch.empty(sh.n_layers, sh.n_kv_heads, n, sh.dim, dtype=self.kv_dtype,
+                               device=self.device)
+            values = torch.empty_like(keys)
+            for layer in range(sh.n_layers):
+                kp = [ctx_dir / f"L{layer}H{h}.k.avdb" for h in range(sh.n_kv_heads)]
+                vp = [ctx_dir / f"L{layer}H{h}.v.avdb" for h in range(sh.n_kv_heads)]
+                vfs.load_to_device(kp, n, sh.dim, self.kv_dtype, self.device, out=keys[layer])
+                vfs.load_to_device(vp, n, sh.dim, self.kv_dtype, self.device, out=values[layer])
+            record = ContextRecord(meta["context_id"], token_ids, keys, values, sh,
+                                   self._plans_for(n))
+            self._build_indexes(record)
+            self.contexts[record.context_id] = record
 
     def _build_indexes(self, record: ContextRecord) -> None:
         """Per (layer, kv head) index kinds from the plans (``store.py:497-521``):

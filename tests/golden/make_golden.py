@@ -181,6 +181,60 @@ def topk_known_answers():
     print("topk_known_answers")
 
 
+AVDB_HASH_CASES = [  # (name, n, dim, element_width, seed): sha256 of the reference's bytes
+    ("empty32", 0, 16, 32, 1), ("one32", 1, 16, 32, 2), ("small32", 37, 16, 32, 3),
+    ("multi32", 300, 32, 32, 4), ("small16", 37, 16, 16, 5), ("multi16", 500, 128, 16, 6),
+    ("dirchain32", 20000, 16, 32, 7), ("edge16", 64, 16, 16, 8),
+]
+
+
+def avdb_vectors(n, dim, seed, width):
+    rng = np.random.default_rng(seed)
+    v = (rng.standard_normal((n, dim)) * 3).astype(np.float32)
+    if width == 16 and n:  # exercise rounding ties, overflow and subnormals
+        v[0, :8] = np.array([65504, 65520, 1e-8, 6e-8, -2.98e-8, 1.0009765625, 2 ** -24, -0.0],
+                            dtype=np.float32)
+    return v
+
+
+def avdb_fixtures():
+    """AVDB files written by the real reference (sparsekv/vfs.py)."""
+    import tempfile
+
+    from sparsekv.vfs import append_vectors, delete_vectors, read_vector_file, write_vector_file
+    out = OUT / "avdb"
+    out.mkdir(exist_ok=True)
+    hashes = {}
+    with tempfile.TemporaryDirectory() as td:
+        for name, n, dim, width, seed in AVDB_HASH_CASES:
+            f = Path(td) / f"{name}.avdb"
+            write_vector_file(f, avdb_vectors(n, dim, seed, width), element_width=width)
+            b = f.read_bytes()
+            hashes[name] = (hashlib.sha256(b).hexdigest(), len(b))
+    import json
+    (out / "hashes.json").write_text(json.dumps(
+        {"cases": AVDB_HASH_CASES, "sha256": hashes}, indent=1) + "\n")
+    # mutated files (append + tombstone) and a file with a graph index chain
+    rng = np.random.default_rng(99)
+    v1 = (rng.standard_normal((100, 32))).astype(np.float32)
+    v2 = (rng.standard_normal((150, 32))).astype(np.float32)
+    f = out / "appended_tomb16.avdb"
+    write_vector_file(f, v1, element_width=16)
+    append_vectors(f, v2)
+    delete_vectors(f, [3, 7, 120])
+    c = read_vector_file(f)
+    np.savez_compressed(out / "appended_tomb16.npz", vectors=c.vectors,
+                        tombstones=np.array(sorted(c.tombstones)))
+    adj = [rng.choice(60, size=int(rng.integers(0, 9)), replace=False).astype(np.int32)
+           for _ in range(60)]
+    v3 = (rng.standard_normal((60, 16))).astype(np.float32)
+    f = out / "graph32.avdb"
+    write_vector_file(f, v3, adjacency=adj, entry_point=5, max_degree=8)
+    c = read_vector_file(f)
+    np.savez_compressed(out / "graph32.npz", vectors=c.vectors)
+    print("avdb fixtures")
+
+
 def known_answers():
     """Known-answer DIPR / window cases lifted from the reference's own tests."""
     rng = np.random.default_rng(12345)  # reference tests/conftest.py:7-9
@@ -215,6 +269,7 @@ def known_answers():
 
 def main():
     known_answers()
+    avdb_fixtures()
     topk_known_answers()
     topk_session_case("tiny_topk_flat", "flat", 20, 2, 4, 2, 16, 200, 2, seed=11, win_init=4,
                       win_last=8, clusters=6, store_inputs=True)

@@ -91,3 +91,13 @@ def window_rows(case: SessionCase, step: int, layer: int):
     wk = np.transpose(case.k[: step + 1, layer], (1, 0, 2))
     wv = np.transpose(case.v[: step + 1, layer], (1, 0, 2))
     return np.ascontiguousarray(wk), np.ascontiguousarray(wv)
+
+
+def avdb_vectors(n, dim, seed, width):
+    """Inputs of the AVDB hash fixtures (same as tests/golden/make_golden.py)."""
+    rng = np.random.default_rng(seed)
+    v = (rng.standard_normal((n, dim)) * 3).astype(np.float32)
+    if width == 16 and n:  # exercise rounding ties, overflow and subnormals
+        v[0, :8] = np.array([65504, 65520, 1e-8, 6e-8, -2.98e-8, 1.0009765625, 2 ** -24, -0.0],
+                            dtype=np.float32)
+    return v
