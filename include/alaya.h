@@ -220,6 +220,38 @@ int alaya_sparse_attention(const alaya_params* p, const alaya_seq* seqs, int bat
                            const int32_t* d_count, float* d_out, int32_t* d_selected,
                            int32_t* d_status, void* stream);
 
+/* ---- graph DIPRS (dipr.py:107-289) --------------------------------------- */
+
+/* Proximity graph over one sequence's base prefix, per kv head h (CSR):
+ * neighbours of node u = nbrs[h*nbrs_head_stride + offsets[h*offsets_head_stride + u] ...
+ * offsets[... + u + 1]); entry[h] = entry point. n_nodes must equal the
+ * sequence's n (the reference walks a graph only when p == index.n). */
+typedef struct {
+  const int64_t* offsets;
+  const int32_t* nbrs;
+  const int32_t* entry;
+  int64_t offsets_head_stride;
+  int64_t nbrs_head_stride;
+  int32_t n_nodes;
+  int32_t pad_;
+} alaya_graph;
+
+size_t alaya_diprs_workspace_bytes(const alaya_params* p, const alaya_seq* seqs,
+                                   const alaya_graph* graphs, int batch);
+
+/* diprs(index, q, entry, l0, beta, window_max) per (seq, q head): the
+ * candidate-list walk of traverse() with the reference's acceptance rule, and
+ * the final cut s >= max(best, floor) - beta. floor_mode 0: none; 1: the
+ * window-cache maximum (Session._window_score_max, store.py:339-354: base
+ * window ids + session rows); 2: d_floors[b*Hq+qh]. Ids (global, no order)
+ * into d_ids[(b*Hq+qh)*cap ...], counts into d_count (-1: an adjacency list
+ * exceeded the scratch), explored-node counts into d_explored (nullable).
+ * graphs: host array [batch]. */
+int alaya_diprs(const alaya_params* p, const alaya_seq* seqs, const alaya_graph* graphs, int batch,
+                const float* d_q, int l0, int floor_mode, const float* d_floors, int64_t* d_ids,
+                int64_t cap, int32_t* d_count, int32_t* d_explored, void* d_ws, size_t ws_bytes,
+                void* stream);
+
 /* ---- AVDB vector files (reference vfs.py, docs/file-format.md) ---------- */
 
 typedef struct {
@@ -243,6 +275,12 @@ int alaya_avdb_stat(const char* path, alaya_avdb_info* out);
  * vectors [n][dim], element_width 32 or 16 (half, round-to-nearest-even).
  * Byte-identical to the reference writer. Host only. */
 int alaya_avdb_write(const char* path, const float* vectors, int64_t n, int dim, int element_width);
+
+/* Graph index chain of a K file (vfs.py:126-145, 324-330): sizes, entry point
+ * and max degree; fills degrees [n_nodes] / nbrs [n_edges] (host, nullable:
+ * call once for the sizes). n_nodes = 0 when the file has no index. */
+int alaya_avdb_graph(const char* path, int64_t* n_nodes, int64_t* n_edges, int32_t* entry_point,
+                     int32_t* max_degree, int32_t* degrees, int32_t* nbrs);
 
 /* Pinned staging bytes alaya_avdb_load needs for these files (0 on error). */
 size_t alaya_avdb_staging_bytes(const char* const* paths, int n_files);

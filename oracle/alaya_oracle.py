@@ -362,6 +362,86 @@ def session_attention_topk(q, base_k, base_v, win_k, win_v, k, coarse=False, blo
     return out, sels, counts
 
 
+# --------------------------------------------------------------------------
+# dipr.py: graph DIPRS over a proximity graph (plain walk, no prefix filter)
+# --------------------------------------------------------------------------
+
+class CandidateList:
+    """Append-only candidate list with a capacity threshold -- ``dipr.py:107-158``."""
+
+    def __init__(self, l0: int, beta: float, floor: float = -np.inf):
+        if l0 < 1:
+            raise ValueError(f"capacity threshold must be >= 1, got {l0}")
+        if beta < 0:
+            raise ValueError(f"beta must be non-negative, got {beta}")
+        self.l0, self.beta, self.floor = l0, beta, floor
+        self.ids: list[int] = []
+        self.scores: list[float] = []
+        self.best_score, self.best_id = -np.inf, -1
+
+    def __len__(self) -> int:
+        return len(self.ids)
+
+    def _push(self, token_id, score):
+        self.ids.append(token_id)
+        self.scores.append(score)
+        if score > self.best_score or (score == self.best_score and token_id < self.best_id):
+            self.best_score, self.best_id = score, token_id
+
+    @property
+    def bound(self) -> float:
+        return max(self.best_score, self.floor)
+
+    def try_append(self, token_id, score) -> bool:
+        if len(self.ids) <= self.l0 or score >= self.bound - self.beta:
+            self._push(token_id, score)
+            return True
+        return False
+
+    def result(self) -> set:
+        cut = self.bound - self.beta
+        return {t for t, sc in zip(self.ids, self.scores) if sc >= cut}
+
+
+def diprs(keys, offsets, nbrs, q, start, l0, beta, window_max=None) -> set:
+    """Graph DIPRS -- ``dipr.py:265-289`` via ``traverse`` ``:166-262`` (no
+    ``admitted_limit``): walk the list in insertion order in batches; each
+    batch offers its entries' neighbours (adjacency order, deduplicated keeping
+    the first occurrence), unvisited ones are scored and offered in order.
+    The graph is CSR: neighbours of u = ``nbrs[offsets[u]:offsets[u+1]]``."""
+    n = keys.shape[0]
+    if n == 0:
+        raise ValueError("search over an empty index")
+    if not 0 <= start < n:
+        raise ValueError(f"start node {start} out of range")
+    keys64 = keys.astype(np.float64)
+    q64 = np.asarray(q).astype(np.float64)
+    floor = -np.inf if window_max is None else float(window_max)
+    cands = CandidateList(l0, beta, floor=floor)
+    cands._push(start, float(keys64[start] @ q64))  # CandidateList.seed
+    visited = np.zeros(n, dtype=bool)
+    visited[start] = True
+    cursor = 0
+    while cursor < len(cands):
+        batch = cands.ids[cursor:]
+        cursor = len(cands)
+        pieces = [nbrs[offsets[u]:offsets[u + 1]] for u in batch]
+        offered = np.concatenate(pieces) if pieces else np.empty(0, np.int64)
+        if offered.size == 0:
+            continue
+        _, first = np.unique(offered, return_index=True)
+        first.sort()
+        offered = offered[first]
+        fresh = offered[~visited[offered]]
+        if fresh.size == 0:
+            continue
+        visited[fresh] = True
+        scores = keys64[fresh] @ q64
+        for token_id, score in zip(fresh.tolist(), scores.tolist()):
+            cands.try_append(token_id, score)
+    return cands.result()
+
+
 def block_box_bounds(keys: np.ndarray, block_size: int):
     """Per-block per-dim (min, max) boxes over contiguous blocks.
 

@@ -38,7 +38,7 @@ EXPORTS = (
     "alaya_ws_status", "alaya_window_append", "alaya_block_bounds", "alaya_ws_block_stats",
     "alaya_ws_candidate_counts", "alaya_topk", "alaya_block_reps", "alaya_block_topk",
     "alaya_sparse_attention", "alaya_avdb_stat", "alaya_avdb_write", "alaya_avdb_staging_bytes",
-    "alaya_avdb_load",
+    "alaya_avdb_load", "alaya_avdb_graph", "alaya_diprs", "alaya_diprs_workspace_bytes",
 )
 
 
@@ -85,6 +85,16 @@ class AlayaAvdbInfo(ctypes.Structure):
         ("n_index_blocks", ctypes.c_uint32), ("n_tombstones", ctypes.c_uint32),
         ("pad_", ctypes.c_uint32), ("file_bytes", ctypes.c_uint64),
         ("directory_offset", ctypes.c_uint64), ("index_head", ctypes.c_uint64),
+    ]
+
+
+class AlayaGraph(ctypes.Structure):
+    """``alaya_graph`` (include/alaya.h)."""
+
+    _fields_ = [
+        ("offsets", ctypes.c_void_p), ("nbrs", ctypes.c_void_p), ("entry", ctypes.c_void_p),
+        ("offsets_head_stride", ctypes.c_int64), ("nbrs_head_stride", ctypes.c_int64),
+        ("n_nodes", ctypes.c_int32), ("pad_", ctypes.c_int32),
     ]
 
 
@@ -151,6 +161,13 @@ def load() -> ctypes.CDLL:
     lib.alaya_avdb_staging_bytes.argtypes = [cpp, i32]
     lib.alaya_avdb_load.restype = i32
     lib.alaya_avdb_load.argtypes = [cpp, i32, i64, i32, i32, vp, i64, vp, sz, vp]
+    G = ctypes.POINTER(AlayaGraph)
+    lib.alaya_avdb_graph.restype = i32
+    lib.alaya_avdb_graph.argtypes = [cp, vp, vp, vp, vp, vp, vp]
+    lib.alaya_diprs_workspace_bytes.restype = sz
+    lib.alaya_diprs_workspace_bytes.argtypes = [P, S, G, i32]
+    lib.alaya_diprs.restype = i32
+    lib.alaya_diprs.argtypes = [P, S, G, i32, vp, i32, i32, vp, vp, i64, vp, vp, vp, sz, vp]
     lib.alaya_ws_status.restype = vp
     lib.alaya_ws_status.argtypes = [vp]
     _lib = lib

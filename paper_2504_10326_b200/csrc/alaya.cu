@@ -454,6 +454,41 @@ int alaya_block_topk(const alaya_params* p, const alaya_seq* seqs, const alaya_b
                            d_blocks, d_block_scores, static_cast<cudaStream_t>(stream));
 }
 
+size_t alaya_diprs_workspace_bytes(const alaya_params* p, const alaya_seq* seqs,
+                                   const alaya_graph* graphs, int batch) {
+  static thread_local Batch bt;
+  if (!graphs || build_batch(p, seqs, batch, &bt) != ALAYA_OK) return 0;
+  int max_n = 1;
+  for (int b = 0; b < batch; ++b) max_n = std::max(max_n, graphs[b].n_nodes);
+  return (size_t)diprs_row_bytes(max_n, kDiprsCap) * batch * p->n_query_heads;
+}
+
+int alaya_diprs(const alaya_params* p, const alaya_seq* seqs, const alaya_graph* graphs, int batch,
+                const float* d_q, int l0, int floor_mode, const float* d_floors, int64_t* d_ids,
+                int64_t cap, int32_t* d_count, int32_t* d_explored, void* d_ws, size_t ws_bytes,
+                void* stream) {
+  static thread_local Batch bt;
+  int rc = build_batch(p, seqs, batch, &bt);
+  if (rc) return rc;
+  if (!graphs || !d_q || !d_ids || !d_count || !d_ws) return fail(ALAYA_ERR_ARG, "null graphs/q/ids/count/ws");
+  if (l0 < 1) return fail(ALAYA_ERR_ARG, "capacity threshold must be >= 1, got %d", l0);
+  if (floor_mode < 0 || floor_mode > 2 || (floor_mode == 2 && !d_floors))
+    return fail(ALAYA_ERR_ARG, "bad floor mode");
+  for (int b = 0; b < batch; ++b) {
+    const alaya_graph& g = graphs[b];
+    if (seqs[b].token_offset != 0 || seqs[b].prefix_len != seqs[b].n)
+      return fail(ALAYA_ERR_UNSUPPORTED, "graph DIPRS runs on unsharded sequences");
+    if (g.n_nodes != seqs[b].n || g.n_nodes < 1)
+      return fail(ALAYA_ERR_ARG, "seq %d: graph of %d nodes over a prefix of %d tokens", b, g.n_nodes,
+                  seqs[b].n);
+    if (!g.offsets || !g.nbrs || !g.entry) return fail(ALAYA_ERR_ARG, "seq %d: null graph arrays", b);
+    if (g.offsets_head_stride < (int64_t)g.n_nodes + 1) return fail(ALAYA_ERR_SHAPE, "seq %d: offsets stride", b);
+  }
+  if (cap < 1) return fail(ALAYA_ERR_ARG, "cap must be >= 1");
+  return launch_diprs(bt, p->dtype, graphs, d_q, l0, floor_mode, d_floors, kDiprsCap, d_ids, cap, d_count,
+                      d_explored, d_ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
 int alaya_sparse_attention(const alaya_params* p, const alaya_seq* seqs, int batch,
                            const float* d_q, const int64_t* d_ids, int64_t cap,
                            const int32_t* d_count, float* d_out, int32_t* d_selected,

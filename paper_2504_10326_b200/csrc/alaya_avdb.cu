@@ -266,6 +266,52 @@ int alaya_avdb_write(const char* path, const float* vectors, int64_t n, int dim,
   return ALAYA_OK;
 }
 
+int alaya_avdb_graph(const char* path, int64_t* n_nodes, int64_t* n_edges, int32_t* entry_point,
+                     int32_t* max_degree, int32_t* degrees, int32_t* nbrs) {
+  if (!path || !n_nodes || !n_edges || !entry_point || !max_degree) return fail(ALAYA_ERR_ARG, "null outputs");
+  alaya_avdb_info info;
+  std::vector<Dir> dir;
+  int rc = parse(path, &info, &dir);
+  if (rc) return rc;
+  *n_nodes = *n_edges = 0;
+  *entry_point = *max_degree = 0;
+  if (info.n_index_blocks == 0) return ALAYA_OK;
+  // the index chain's logical stream (vfs.py:126-145, index blocks in directory order)
+  std::vector<uint8_t> stream;
+  const int fd = open(path, O_RDONLY);
+  if (fd < 0) return fail(ALAYA_ERR_ARG, "%s: cannot open", path);
+  uint8_t blk[kBlock];
+  for (const Dir& d : dir) {
+    if (d.type != kIndex) continue;
+    if ((rc = read_exact(fd, d.offset, blk, kBlock, path))) { close(fd); return rc; }
+    const uint32_t len = rd<uint32_t>(blk + 4);
+    if (blk[0] != kIndex || len > kPayload) { close(fd); return fail(ALAYA_ERR_ARG, "%s @ %llu: bad index block", path, (unsigned long long)d.offset); }
+    stream.insert(stream.end(), blk + kBlockHdr, blk + kBlockHdr + len);
+  }
+  close(fd);
+  if (stream.size() < 12) return fail(ALAYA_ERR_ARG, "%s: truncated index stream", path);
+  const uint32_t ep = rd<uint32_t>(stream.data()), md = rd<uint32_t>(stream.data() + 4);
+  const uint32_t nn = rd<uint32_t>(stream.data() + 8);
+  if (stream.size() < 12 + 4ull * nn) return fail(ALAYA_ERR_ARG, "%s: truncated degree table", path);
+  uint64_t ne = 0;
+  for (uint32_t i = 0; i < nn; ++i) ne += rd<uint32_t>(stream.data() + 12 + 4ull * i);
+  if (stream.size() < 12 + 4ull * nn + 4ull * ne) return fail(ALAYA_ERR_ARG, "%s: truncated neighbour list", path);
+  *n_nodes = nn;
+  *n_edges = (int64_t)ne;
+  *entry_point = (int32_t)ep;
+  *max_degree = (int32_t)md;
+  if (degrees) memcpy(degrees, stream.data() + 12, 4ull * nn);
+  if (nbrs) {
+    const uint8_t* fl = stream.data() + 12 + 4ull * nn;
+    for (uint64_t e = 0; e < ne; ++e) {
+      const uint32_t v = rd<uint32_t>(fl + 4 * e);
+      if (v >= info.n_vectors) return fail(ALAYA_ERR_ARG, "%s @ 0: node references a missing vector slot", path);
+      nbrs[e] = (int32_t)v;
+    }
+  }
+  return ALAYA_OK;
+}
+
 size_t alaya_avdb_staging_bytes(const char* const* paths, int n_files) {
   size_t tot = 0;
   for (int i = 0; i < n_files; ++i) {

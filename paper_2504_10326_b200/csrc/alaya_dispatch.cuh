@@ -128,6 +128,11 @@ int launch_tc_scan(const Batch& bt, const alaya_seq* seqs, const float* q, const
 int launch_tc_fused(const Batch& bt, const alaya_seq* seqs, const float* q, const Ws& ws,
                     cudaStream_t st);
 bool fused_enabled();
+int64_t diprs_row_bytes(int max_n, int cap);
+int launch_diprs(const Batch& bt, int dtype, const alaya_graph* graphs, const float* q, int l0, int floor_mode,
+                 const float* floors, int cap, int64_t* ids, int64_t out_cap, int32_t* count, int32_t* explored,
+                 void* ws, size_t ws_bytes, cudaStream_t st);
+constexpr int kDiprsCap = 32768;  // offered ids per sub-batch (per row scratch)
 int launch_topk_select(const Batch& bt, const Ws& ws, int k, int64_t* ids, float* scores, int64_t cap,
                        int32_t* count, cudaStream_t st);
 int launch_sparse_attention(const Batch& bt, int dtype, const float* q, const int64_t* ids, int64_t cap,

@@ -73,3 +73,37 @@ def dipr_bruteforce(q, keys, beta: float, token_ids: Iterable[int] | None = None
     if tid.shape[0] != n:
         raise ValueError("token_ids length must match key count")
     return set(tid[ids].tolist())
+
+
+def diprs(index, q, start: int, l0: int, beta: float, window_max: float | None = None) -> set[int]:
+    """Approximate DIPR over a proximity graph (``dipr.py:265-289``): the
+    candidate-list walk of ``traverse`` on the GPU (``alaya_diprs``), with the
+    reference's acceptance rule and final cut ``s >= max(best, floor) - beta``."""
+    engine.require_cuda()
+    if l0 < 1:
+        raise ValueError(f"capacity threshold must be >= 1, got {l0}")
+    if beta < 0:
+        raise ValueError(f"beta must be non-negative, got {beta}")
+    n = index.n
+    if n == 0:
+        raise ValueError("search over an empty index")
+    if not 0 <= start < n:
+        raise ValueError(f"start node {start} out of range")
+    k = index.keys
+    d = k.shape[1]
+    dev = k.device
+    params = engine.make_params(1, 1, d, k.dtype, beta, 0, 0)
+    call = engine.Call([engine.SeqView(k=k.unsqueeze(0), v=k.unsqueeze(0), n=n)], params, k.dtype, dev)
+    qt = torch.as_tensor(np.asarray(q, dtype=np.float32) if not isinstance(q, torch.Tensor) else q)
+    qt = qt.to(device=dev, dtype=torch.float32).reshape(1, 1, d)
+    floors = None if window_max is None else torch.tensor([float(window_max)], device=dev)
+    ids, cnt, _ = call.diprs(qt, [index.device_arrays(start)], l0, 0 if floors is None else 2, floors)
+    c = int(cnt[0].item())
+    if c < 0:
+        raise _lib_error("graph walk scratch overflow")
+    return set(ids[0, :c].cpu().numpy().tolist())
+
+
+def _lib_error(msg):
+    from ._lib import AlayaError
+    return AlayaError(msg)

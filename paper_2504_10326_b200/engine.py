@@ -23,7 +23,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import AlayaBlockIndex, AlayaParams, AlayaSeq, check
+from ._lib import AlayaBlockIndex, AlayaGraph, AlayaParams, AlayaSeq, check
 
 _DTYPES = {torch.float32: _lib.ALAYA_F32, torch.bfloat16: _lib.ALAYA_BF16}
 
@@ -120,6 +120,7 @@ class _Workspace(threading.local):
 
 
 _WS = _Workspace()
+_DWS = _Workspace()  # graph-walk scratch (separate from the scan workspace)
 
 
 class Call:
@@ -262,6 +263,42 @@ class Call:
                                         sc.data_ptr() if sc is not None else None, self.stream))
         self._q_keep = q
         return (ids, cnt, blk, sc) if with_blocks else (ids, cnt)
+
+    def diprs(self, q: torch.Tensor, graphs: list, l0: int, floor_mode: int = 0,
+              floors: torch.Tensor | None = None):
+        """Graph DIPRS per (seq, q head) (``dipr.py:265-289``): ``graphs[b]`` =
+        ``(offsets [Hkv, n+1] int64, nbrs [Hkv, E] int32, entry [Hkv] int32)`` over
+        sequence b's prefix. floor_mode 0 none, 1 window-cache max, 2 ``floors``.
+        Returns ``(ids [rows, n] int64 (unordered), counts, explored)``."""
+        q = self._q(q)
+        rows = self.B * self.params.n_query_heads
+        arr = (AlayaGraph * self.B)()
+        keep = []
+        for i, (off, nb, ent) in enumerate(graphs):
+            if off.dtype != torch.int64 or nb.dtype != torch.int32 or ent.dtype != torch.int32:
+                raise ValueError("graph arrays must be int64 offsets, int32 nbrs and entry")
+            off, nb, ent = off.contiguous(), nb.contiguous(), ent.contiguous()
+            keep += [off, nb, ent]
+            arr[i].offsets, arr[i].nbrs, arr[i].entry = off.data_ptr(), nb.data_ptr(), ent.data_ptr()
+            arr[i].offsets_head_stride, arr[i].nbrs_head_stride = off.stride(0), max(1, nb.stride(0))
+            arr[i].n_nodes = off.shape[1] - 1
+        cap = max(1, max(int(self.seqs[i].n) for i in range(self.B)))
+        nbytes = self.lib.alaya_diprs_workspace_bytes(ctypes.byref(self.params), self.seqs, arr, self.B)
+        if nbytes == 0:
+            check(_lib.ALAYA_ERR_ARG)
+        ws = self.ws if self.ws.numel() >= nbytes else _DWS.get(nbytes, self.device)
+        ids = torch.empty(rows, cap, dtype=torch.int64, device=self.device)
+        cnt = torch.empty(rows, dtype=torch.int32, device=self.device)
+        exp = torch.empty(rows, dtype=torch.int32, device=self.device)
+        fl = None
+        if floor_mode == 2:
+            fl = floors.to(device=self.device, dtype=torch.float32).contiguous()
+        check(self.lib.alaya_diprs(ctypes.byref(self.params), self.seqs, arr, self.B, q.data_ptr(),
+                                   int(l0), int(floor_mode), fl.data_ptr() if fl is not None else None,
+                                   ids.data_ptr(), cap, cnt.data_ptr(), exp.data_ptr(), ws.data_ptr(),
+                                   ws.numel(), self.stream))
+        self._q_keep = (q, keep, fl)
+        return ids, cnt, exp
 
     def sparse_attention(self, q: torch.Tensor, ids: torch.Tensor, counts: torch.Tensor,
                          out: torch.Tensor | None = None):

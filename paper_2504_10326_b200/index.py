@@ -5,7 +5,8 @@ here the keys stay in HBM in their storage dtype and the scan kernel
 accumulates in fp32. ``BlockIndex`` (``index.py:195-243``) holds the
 representatives as one device tensor ``[blocks, r, d]`` built by
 ``alaya_block_reps``; ``top_blocks`` runs ``alaya_block_topk``.
-Graph construction is out of scope.
+``GraphIndex`` holds a proximity graph as device CSR for ``dipr.diprs``
+(``alaya_diprs``); graph construction is out of scope.
 """
 
 from __future__ import annotations
@@ -105,6 +106,72 @@ class BlockIndex:
         blk, sc = blk[keep], sc[keep]
         order = np.lexsort((blk, -sc.astype(np.float64)))
         return [(int(self.starts[i]), int(self.ends[i])) for i in blk[order]]
+
+
+class GraphIndex:
+    """Fixed-max-degree proximity graph over one head's keys (``index.py:73-192``),
+    held on the device as CSR: ``offsets [n+1]`` int64, ``nbrs`` int32. Built
+    by the reference (``build_graph``) and persisted in AVDB index blocks, or
+    given as arrays (``from_arrays``); graph construction itself is out of
+    scope on the B200 engine."""
+
+    def __init__(self, keys, adjacency, entry_point: int, max_degree: int, device=None):
+        dev = torch.device(device or "cuda")
+        self.keys = _device_keys(keys, dev)
+        adjacency = [np.asarray(a, dtype=np.int32) for a in adjacency]
+        degrees = np.array([a.size for a in adjacency], dtype=np.int64)
+        flat = np.concatenate(adjacency) if degrees.sum() else np.empty(0, np.int32)
+        self._set(degrees, flat, entry_point, max_degree)
+
+    def _set(self, degrees, flat, entry_point, max_degree):
+        dev = self.keys.device
+        n = self.keys.shape[0]
+        if degrees.shape[0] != n:
+            raise ValueError("adjacency length != node count")
+        if flat.size and (flat.min() < 0 or flat.max() >= n):
+            raise ValueError("neighbour id out of range")
+        if not 0 <= entry_point < n:
+            raise ValueError("entry point out of range")
+        off = np.zeros(n + 1, dtype=np.int64)
+        off[1:] = np.cumsum(degrees)
+        self.offsets = torch.from_numpy(off).to(dev)
+        pad = flat if flat.size else np.zeros(1, np.int32)  # a C-ABI pointer even without edges
+        self.nbrs = torch.from_numpy(np.ascontiguousarray(pad, dtype=np.int32)).to(dev)
+        self.entry_point = int(entry_point)
+        self.max_degree = int(max_degree)
+        self._degrees = degrees.astype(np.int32)
+        self._flat = np.ascontiguousarray(flat, dtype=np.int32)
+
+    @classmethod
+    def from_arrays(cls, keys, degrees, flat_neighbors, entry_point, max_degree, device=None):
+        """``index.py:172-188``."""
+        self = cls.__new__(cls)
+        self.keys = _device_keys(keys, torch.device(device or "cuda"))
+        self._set(np.asarray(degrees, dtype=np.int64), np.asarray(flat_neighbors, dtype=np.int32),
+                  entry_point, max_degree)
+        return self
+
+    def to_arrays(self):
+        return self._degrees.copy(), self._flat.copy()
+
+    @property
+    def n(self) -> int:
+        return self.keys.shape[0]
+
+    @property
+    def adjacency(self) -> list[np.ndarray]:
+        off = self.offsets.cpu().numpy()
+        return [self._flat[off[i]:off[i + 1]] for i in range(self.n)]
+
+    def neighbors(self, node: int) -> np.ndarray:
+        off = self.offsets[node:node + 2].cpu().numpy()
+        return self._flat[off[0]:off[1]]
+
+    def device_arrays(self, start: int | None = None):
+        """``(offsets [1, n+1], nbrs [1, E], entry [1])`` for ``Call.diprs``."""
+        ent = torch.tensor([self.entry_point if start is None else int(start)], dtype=torch.int32,
+                           device=self.keys.device)
+        return self.offsets.unsqueeze(0), self.nbrs.unsqueeze(0), ent
 
 
 def select_representatives(block_keys, r: int) -> np.ndarray:

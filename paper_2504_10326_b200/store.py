@@ -69,6 +69,7 @@ class ContextRecord:
     indexes: dict = field(default_factory=dict)
     bounds: torch.Tensor | None = None  # [L, Hkv, blocks, 2, d] coarse block index (block filter)
     block_reps: dict = field(default_factory=dict)  # layer -> [Hkv, blocks, r, d] (BlockIndex)
+    graphs: dict = field(default_factory=dict)  # layer -> (offsets [Hkv,n+1], nbrs [Hkv,E], entry [Hkv])
 
     @property
     def length(self) -> int:
@@ -238,7 +239,7 @@ class Session:
                               device=st.device)
         calls = []
         for key, idx in groups.items():
-            if key[0] == "topk":
+            if key[0] in ("topk", "diprs"):
                 for c0 in range(0, len(idx), _lib.MAX_BATCH):
                     part = idx[c0:c0 + _lib.MAX_BATCH]
                     Session._topk_group([sessions[i] for i in part], part, key, layer, qd, out)
@@ -276,13 +277,22 @@ class Session:
         """TOP_K plans (``store.py:305-318``) for sessions sharing (k, mode):
         flat exact top-k or coarse block top-k, then sparse attention over the
         retrieved ids (``store.py:268-293``)."""
-        _, k, coarse, wi, wl = key
         st = sessions[0]._store
-        call = st._call_for(sessions, layer, 0.0, wi, wl)
+        if key[0] == "diprs":  # graph DIPRS (store.py:330-333)
+            _, beta, wi, wl = key
+            call = st._call_for(sessions, layer, beta, wi, wl)
+        else:
+            _, k, coarse, wi, wl = key
+            call = st._call_for(sessions, layer, 0.0, wi, wl)
         full = len(rows) == out.shape[0]
         sel = None if full else torch.tensor(rows, device=st.device)
         qs = qd if full else qd.index_select(0, sel)
-        if coarse:
+        if key[0] == "diprs":
+            ids, cnt, _ = call.diprs(qs, [s.base.graphs[layer] for s in sessions], st.config.l0,
+                                     floor_mode=1)
+            if int(cnt.min().item()) < 0:
+                raise _lib.AlayaError("graph walk scratch overflow")
+        elif coarse:
             bs = st.config.block_size
             want = max(1, -(-k // bs))  # store.py:307
             idxs = [(s.base.block_reps[layer], s.base.length) for s in sessions]
@@ -365,6 +375,10 @@ class Session:
                       and self.reused_prefix_len > 0)
             return ("topk", k, bool(coarse), cfg.window_initial, cfg.window_last)
         beta = active.beta if active.beta is not None else cfg.beta
+        if (active.query is QueryKind.DIPR and self.base is not None and layer in self.base.graphs
+                and self.reused_prefix_len == self.base.length):
+            # graph index and p == index.n: DIPRS with the window-cache floor
+            return ("diprs", float(beta), cfg.window_initial, cfg.window_last)
         return ("dipr", float(beta), cfg.window_initial, cfg.window_last)
 
     def active_plan(self, layer: int) -> Plan:
@@ -525,15 +539,36 @@ class ContextStore:
             keys = torch.empty(sh.n_layers, sh.n_kv_heads, n, sh.dim, dtype=self.kv_dtype,
                                device=self.device)
             values = torch.empty_like(keys)
+            graphs = {}
             for layer in range(sh.n_layers):
                 kp = [ctx_dir / f"L{layer}H{h}.k.avdb" for h in range(sh.n_kv_heads)]
                 vp = [ctx_dir / f"L{layer}H{h}.v.avdb" for h in range(sh.n_kv_heads)]
                 vfs.load_to_device(kp, n, sh.dim, self.kv_dtype, self.device, out=keys[layer])
                 vfs.load_to_device(vp, n, sh.dim, self.kv_dtype, self.device, out=values[layer])
+                g = [vfs.read_graph(f) for f in kp]
+                if all(x is not None for x in g):
+                    graphs[layer] = self._stack_graphs(g, n)
             record = ContextRecord(meta["context_id"], token_ids, keys, values, sh,
                                    self._plans_for(n))
             self._build_indexes(record)
+            record.graphs = graphs
             self.contexts[record.context_id] = record
+
+    def _stack_graphs(self, heads: list, n: int):
+        """Per-head (degrees, flat, entry, max_degree) -> stacked device CSR."""
+        emax = max(1, max(int(f.size) for _, f, _, _ in heads))
+        off = np.zeros((len(heads), n + 1), dtype=np.int64)
+        nb = np.zeros((len(heads), emax), dtype=np.int32)
+        ent = np.zeros(len(heads), dtype=np.int32)
+        for h, (deg, flat, ep, _) in enumerate(heads):
+            if deg.size != n:
+                raise ValueError(f"graph of {deg.size} nodes over {n} tokens")
+            off[h, 1:] = np.cumsum(deg)
+            nb[h, : flat.size] = flat
+            ent[h] = ep
+        dev = self.device
+        return (torch.from_numpy(off).to(dev), torch.from_numpy(nb).to(dev),
+                torch.from_numpy(ent).to(dev))
 
     def _build_indexes(self, record: ContextRecord) -> None:
         """Per (layer, kv head) index kinds from the plans (``store.py:497-521``):

@@ -148,3 +148,21 @@ def read_vector_file(path, device="cuda", dtype=torch.float32) -> VectorFileCont
     h = read_header(path)
     v = load_to_device([path], h.n_vectors, h.dim, dtype, torch.device(device))[0]
     return VectorFileContents(h.dim, h.element_width, v, h.n_tombstones)
+
+
+def read_graph(path):
+    """Adjacency of a file's index chain (``vfs.py:126-145``) as
+    ``(degrees int32 [n], flat int32 [E], entry_point, max_degree)``, or None."""
+    lib = _lib.load()
+    nn, ne = ctypes.c_int64(), ctypes.c_int64()
+    ep, md = ctypes.c_int32(), ctypes.c_int32()
+    p = os.fsencode(path)
+    _check(lib.alaya_avdb_graph(p, ctypes.byref(nn), ctypes.byref(ne), ctypes.byref(ep),
+                                ctypes.byref(md), None, None))
+    if nn.value == 0:
+        return None
+    deg = np.empty(nn.value, dtype=np.int32)
+    flat = np.empty(max(ne.value, 1), dtype=np.int32)
+    _check(lib.alaya_avdb_graph(p, ctypes.byref(nn), ctypes.byref(ne), ctypes.byref(ep),
+                                ctypes.byref(md), deg.ctypes.data, flat.ctypes.data))
+    return deg, flat[: ne.value], int(ep.value), int(md.value)

@@ -235,6 +235,78 @@ def avdb_fixtures():
     print("avdb fixtures")
 
 
+def graph_fixtures():
+    """Graph DIPRS on reference-built graphs (sparsekv index.py build_graph,
+    dipr.py diprs), plus a reference-persisted context whose FINE layer runs
+    DIPRS inside Session.attention."""
+    import shutil
+    import tempfile
+
+    from sparsekv.dipr import diprs
+    from sparsekv.index import GraphParams, build_graph
+    from sparsekv.workload import make_queries
+    cases = {}
+    # reference tests/test_dipr.py:192-205 setup (2000 tokens, d=32)
+    shape = ModelShape(1, 1, 1, 32)
+    spec = WorkloadSpec(n_tokens=2000, shape=shape, seed=21)
+    ctx = make_context(spec)
+    keys = ctx.keys[0, 0]
+    g = build_graph(keys, make_queries(spec, 800, ctx.centers, stream=5), GraphParams(enhance_ef=48))
+    deg, flat = g.to_arrays()
+    test_q = make_queries(spec, 30, ctx.centers, stream=6)
+    cases.update(keys=keys, degrees=deg, nbrs=flat, entry=np.int64(g.entry_point), q=test_q)
+    smax = (keys.astype(np.float64) @ test_q.astype(np.float64).T).max(axis=0)
+    runs = []  # (beta, l0, window offset or nan)
+    for beta in (0.0, 1.0, 6.0, 20.0):
+        for l0 in (8, 128):
+            runs.append((beta, l0, np.nan))
+    runs += [(6.0, 128, -0.5), (6.0, 128, 3.0), (20.0, 16, 1.0)]
+    sel, off = [], [0]
+    for beta, l0, wo in runs:
+        for i, q in enumerate(test_q):
+            wm = None if np.isnan(wo) else float(smax[i] + wo)
+            sel.extend(sorted(diprs(g, q, g.entry_point, l0, beta, window_max=wm)))
+            off.append(len(sel))
+    cases["runs"] = np.array(runs)
+    cases["sel"], cases["sel_off"] = np.array(sel, np.int64), np.array(off)
+    np.savez_compressed(OUT / "graph_diprs.npz", **cases)
+    # a persisted context with graph indexes (layer 1 = FINE, layer 0 = FLAT)
+    shape = ModelShape(2, 4, 2, 16)
+    cfg = EngineConfig(window_initial=4, window_last=8, l0=64, beta=8.0, max_degree=8, knn_k=8,
+                       enhance_ef=16, short_context_threshold=64)
+    spec = WorkloadSpec(n_tokens=300, shape=shape, seed=31, clusters=6)
+    ctx = make_context(spec)
+    queries = np.stack([np.stack([make_queries(spec, 40, ctx.centers, stream=10 + 4 * layer + qh)
+                                  for qh in range(4)]) for layer in range(2)])
+    root = OUT / "ctx_graph"
+    if root.exists():
+        shutil.rmtree(root)
+    with tempfile.TemporaryDirectory() as td:
+        db = ContextStore(shape, cfg, root=td)
+        cid = db.import_context(ctx.token_ids, ctx.keys, ctx.values, queries)
+        shutil.copytree(Path(td) / "contexts", root / "contexts")
+    session, _ = db.create_session(ctx.token_ids)
+    tids, qs, ks, vs = decode_step_inputs(spec, 3, ctx.centers)
+    outs, sel, off, ret = [], [], [0], []
+    for step in range(3):
+        for layer in range(2):
+            session.update(qs[step, layer], ks[step, layer], vs[step, layer], layer)
+        for layer in range(2):
+            o = session.attention(qs[step, layer], layer)
+            outs.append(o)
+            for info in session.last_diagnostics["heads"]:
+                sel.extend(info["selected_base"])
+                off.append(len(sel))
+                ret.append(info["retrieved"])
+        plans = [session.active_plan(layer).index.value for layer in range(2)]
+    assert plans == ["flat", "fine"], plans
+    np.savez_compressed(OUT / "ctx_graph_session.npz", out=np.stack(outs), sel=np.array(sel, np.int64),
+                        sel_off=np.array(off), retrieved=np.array(ret), q=qs, k=ks, v=vs,
+                        keys=ctx.keys, values=ctx.values, tokens=ctx.token_ids,
+                        context_id=np.array(cid))
+    print("graph fixtures")
+
+
 def known_answers():
     """Known-answer DIPR / window cases lifted from the reference's own tests."""
     rng = np.random.default_rng(12345)  # reference tests/conftest.py:7-9
@@ -270,6 +342,7 @@ def known_answers():
 def main():
     known_answers()
     avdb_fixtures()
+    graph_fixtures()
     topk_known_answers()
     topk_session_case("tiny_topk_flat", "flat", 20, 2, 4, 2, 16, 200, 2, seed=11, win_init=4,
                       win_last=8, clusters=6, store_inputs=True)

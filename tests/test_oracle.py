@@ -134,3 +134,38 @@ def test_topk_session_bit_exact_vs_reference(name):
             for qh in range(c.hq):
                 assert np.array_equal(sels[qh], c.selected(step, li, qh))
                 assert counts[qh] == c.retrieved[idx * c.hq + qh]
+
+
+# --------------------------------------------------------------------------
+# graph DIPRS (dipr.py:107-289) on reference-built graphs
+# --------------------------------------------------------------------------
+
+def csr(degrees, flat):
+    off = np.zeros(degrees.size + 1, np.int64)
+    off[1:] = np.cumsum(degrees)
+    return off, flat.astype(np.int64)
+
+
+def test_diprs_restatement_vs_reference():
+    z = np.load(GOLDEN / "graph_diprs.npz")
+    keys, q = z["keys"], z["q"]
+    off, nb = csr(z["degrees"], z["nbrs"])
+    smax = (keys.astype(np.float64) @ q.astype(np.float64).T).max(axis=0)
+    so = z["sel_off"]
+    i = 0
+    for beta, l0, wo in z["runs"]:
+        for j in range(q.shape[0]):
+            wm = None if np.isnan(wo) else float(smax[j] + wo)
+            got = sorted(O.diprs(keys, off, nb, q[j], int(z["entry"]), int(l0), float(beta), wm))
+            assert got == z["sel"][so[i]:so[i + 1]].tolist(), (beta, l0, wo, j)
+            i += 1
+
+
+def test_diprs_complete_graph_is_exact(rng):
+    """reference tests/test_dipr.py:184-190: a complete graph gives the brute-force set."""
+    keys = rng.integers(-5, 6, size=(12, 4)).astype(np.float32)
+    q = rng.integers(-5, 6, size=4).astype(np.float32)
+    nb = np.concatenate([[v for v in range(12) if v != u] for u in range(12)])
+    off = np.arange(0, 12 * 11 + 1, 11)
+    for beta in (0.0, 2.0, 10.0):
+        assert O.diprs(keys, off, nb, q, 0, 16, beta) == O.dipr_bruteforce(q, keys, beta)
