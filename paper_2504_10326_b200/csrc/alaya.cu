@@ -334,6 +334,12 @@ int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch
     if ((rc = launch_tc_fused(c.bt, c.seqs, d_q, c.ws, c.stream))) return rc;
     return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);
   }
+  if (c.use_tc && overlap_enabled(c.bt.B * c.bt.Hkv)) {  // attend runs beside the scan (per-group readiness)
+    c.bt.overlap = 1;
+    if ((rc = run_scan(c, d_q))) return rc;
+    if ((rc = c.st.attend_ovl(c.bt, d_q, c.ws, c.stream))) return rc;
+    return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);
+  }
   if ((rc = run_scan(c, d_q))) return rc;  // prep zeroed the status word and the ticket
   if ((rc = c.st.attend(c.bt, d_q, nullptr, c.ws, 1, c.stream, 0))) return rc;
   return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);

@@ -46,6 +46,7 @@ struct Batch {
   int32_t block_filter;
   int32_t split;  // attend task split threshold (candidates per (chunk, head) pair)
   int32_t seed;   // prep_kernel seeds the running max from sampled keys
+  int32_t overlap;  // scan publishes per-group completion; attend runs beside it (PDL)
 };
 
 // Coarse block indexes of a batch (kernel-parameter space).
@@ -86,6 +87,12 @@ struct Ws {
 // launch early (its CTAs then park in their own pdl_wait()).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ uint32_t enc_max(float f) {
   uint32_t u = __float_as_uint(f);

@@ -67,6 +67,18 @@ struct Stages {
     return launch_pdl("attend_kernel", attend_kernel<T, D, G>, (unsigned)blocks, kThreads, 0, st, bt, q,
                       smax, ws, want_values);
   }
+  // attend beside the tcgen05 scan (bt.overlap): PDL dependent, no grid wait
+  static int attend_ovl(const Batch& bt, const float* q, const Ws& ws, cudaStream_t st) {
+    static int per_sm = 0;
+    if (per_sm == 0) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attend_ovl_kernel<T, D, G>, kOvlThreads, 0);
+      if (per_sm < 1) per_sm = 1;
+    }
+    const long tasks = (long)bt.total_chunks * G + (long)bt.B * bt.Hq;
+    const long blocks = std::min<long>((tasks + 3) / 4, (long)per_sm * num_sms());
+    return launch_pdl("attend_ovl_kernel", attend_ovl_kernel<T, D, G>, (unsigned)blocks, kOvlThreads, 0,
+                      st, bt, q, ws);
+  }
   static int filter(const Batch& bt, const float* q, const Ws& ws, cudaStream_t st) {
     if (bt.total_chunks == 0) return ALAYA_OK;
     const int rows = bt.B * bt.Hq;
@@ -95,12 +107,13 @@ struct StageSet {
   CombineFn combine;
   FilterFn filter;
   ScanFn prep;
+  ScanFn attend_ovl;
 };
 
 template <typename T, int D, int G>
 StageSet make_set() {
   return {&Stages<T, D, G>::scan, &Stages<T, D, G>::attend, &Stages<T, D, G>::combine,
-          &Stages<T, D, G>::filter, &Stages<T, D, G>::prep};
+          &Stages<T, D, G>::filter, &Stages<T, D, G>::prep, &Stages<T, D, G>::attend_ovl};
 }
 
 template <typename T, int D>
@@ -128,6 +141,7 @@ int launch_tc_scan(const Batch& bt, const alaya_seq* seqs, const float* q, const
 int launch_tc_fused(const Batch& bt, const alaya_seq* seqs, const float* q, const Ws& ws,
                     cudaStream_t st);
 bool fused_enabled();
+bool overlap_enabled(int groups);
 int64_t diprs_row_bytes(int max_n, int cap);
 int launch_diprs(const Batch& bt, int dtype, const alaya_graph* graphs, const float* q, int l0, int floor_mode,
                  const float* floors, int cap, int64_t* ids, int64_t out_cap, int32_t* count, int32_t* explored,

@@ -470,6 +470,65 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
+// Attend launched BESIDE the tcgen05 scan (bt.overlap): the kernel is a PDL
+// dependent of the scan and skips the grid-dependency wait; the scan only
+// triggers after its own wait, so everything before the scan is complete.
+// A (chunk, head) task starts once its (sequence, kv head) group counter says
+// every epilogue warp of every chunk of the group has published (the group's
+// max is final); heavy pairs' overflow items wait for the whole scan. Window
+// tasks need nothing from the scan and go first.
+constexpr int kOvlThreads = 128;
+
+template <typename T, int D, int G>
+__global__ void __launch_bounds__(kOvlThreads, 4)  // <= 128 regs: one CTA fits beside 3 scan CTAs
+    attend_ovl_kernel(const __grid_constant__ Batch bt, const float* __restrict__ q, Ws ws) {
+  constexpr int W = kOvlThreads / 32;
+  __shared__ int s_t[W][2][32];
+  __shared__ float s_w[W][2][32];
+  pdl_trigger();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwin = bt.B * bt.Hq;
+  const int npairs = bt.total_chunks * G;
+  const int all_done = 4 * bt.total_chunks;
+  int novl = -1;
+  for (;;) {
+    int task = 0;
+    if (lane == 0) task = atomicAdd(&ws.counters[0], 1);
+    task = __shfl_sync(kFull, task, 0);
+    if (task < nwin) {
+      win_task<T, D, G>(bt, q, ws, task, lane);
+      continue;
+    }
+    int qb = 0, qe;
+    size_t cj;
+    if (task < nwin + npairs) {
+      cj = task - nwin;
+      int b, h, ci;
+      decode_chunk(bt, (int)cj / G, b, h, ci);
+      if (lane == 0) {
+        const int* gd = ws.group_done + b * bt.Hkv + h;
+        while (ld_acquire_gpu(gd) < 4 * bt.s[b].nch) __nanosleep(256);
+      }
+      __syncwarp();
+      qe = __ldcg(&ws.heavy[cj]) ? 1 : 4;
+    } else {
+      if (novl < 0) {  // overflow items are final once every chunk has published
+        if (lane == 0) {
+          while (ld_acquire_gpu(&ws.counters[6]) < all_done) __nanosleep(512);
+          novl = __ldcg(&ws.counters[7]);
+        }
+        novl = __shfl_sync(kFull, novl, 0);
+      }
+      if (task - nwin - npairs >= novl) break;
+      const int item = __ldcg(&ws.ovlist[task - nwin - npairs]);
+      cj = (size_t)(item >> 2);
+      qb = item & 3;
+      qe = qb + 1;
+    }
+    sel_task_pipe<T, D, G, true>(bt, nullptr, ws, cj, qb, qe, lane, s_t[warp], s_w[warp], true);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Stage 3: one CTA per (sequence, query head): sum of the chunk partials (the
 // selected set, reference point = max; warps take interleaved chunks, fixed

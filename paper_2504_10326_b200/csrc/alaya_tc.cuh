@@ -266,7 +266,7 @@ __device__ __forceinline__ void mma_tile(uint32_t a_base, uint32_t b_base, uint3
 }
 
 template <int G, int kStages>
-__global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 3 : (kStages <= 3 ? 2 : 1)))
+__global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 4 : (kStages <= 3 ? 2 : 1)))  // 2 stages: <= 80 regs, so 3 CTAs/SM leave room for one attend_ovl CTA
     scan_tc_kernel(const __grid_constant__ Batch bt, const __grid_constant__ Maps maps,
                    const float* __restrict__ q, Ws ws) {
   constexpr int NP = (3 * G <= 16) ? 16 : 32;
@@ -305,8 +305,8 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 3 : (kStages <= 3 
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int chunk = bt.chunk;
-  pdl_trigger();
   pdl_wait();  // gmax seeds and q come from the preceding kernels
+  pdl_trigger();  // after the wait: a dependent launched now sees all earlier work complete
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -413,6 +413,14 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 3 : (kStages <= 3 
       int b, h;
       epilogue_chunk<G, NP>(bt, ws, c, quarter, lane, tmem_base, accf0, acce0, acc, aphase, b, h,
                             tmax, tcount, cur);
+      if (bt.overlap) {  // this warp's candidates, counts, heavy flags and max are
+        __threadfence();  // visible GPU-wide before its group counter moves
+        __syncwarp();
+        if (lane == 0) {
+          atomicAdd(&ws.group_done[b * bt.Hkv + h], 1);
+          atomicAdd(&ws.counters[6], 1);
+        }
+      }
     }
   }
   fence_before();
