@@ -305,8 +305,16 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 4 : (kStages <= 3 
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int chunk = bt.chunk;
-  pdl_wait();  // gmax seeds and q come from the preceding kernels
-  pdl_trigger();  // after the wait: a dependent launched now sees all earlier work complete
+  // The TMA producer streams K (context memory, untouched by the preceding
+  // kernels) without waiting for them, so the first tiles are in flight while
+  // prep_kernel still runs. Every other warp waits (q, gmax seeds, tickets),
+  // then triggers: a dependent launched after the trigger sees all earlier
+  // work complete. (With the block filter the preceding kernel is a plain
+  // launch that never triggers, so this grid starts after it completes.)
+  if (warp != 0) {
+    pdl_wait();
+    pdl_trigger();
+  }
 
   if (warp == 0) {
     // ===================== TMA producer =====================
