@@ -334,7 +334,9 @@ int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch
     if ((rc = launch_tc_fused(c.bt, c.seqs, d_q, c.ws, c.stream))) return rc;
     return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);
   }
-  if (c.use_tc && overlap_enabled(c.bt.B * c.bt.Hkv)) {  // attend runs beside the scan (per-group readiness)
+  // attend beside the scan (per-group readiness); the CUDA-core scan fills the
+  // register file (no room for an attend CTA: measured no gain), so tcgen05 only
+  if (c.use_tc && overlap_enabled(c.bt.B * c.bt.Hkv)) {
     c.bt.overlap = 1;
     if ((rc = run_scan(c, d_q))) return rc;
     if ((rc = c.st.attend_ovl(c.bt, d_q, c.ws, c.stream))) return rc;

@@ -35,15 +35,14 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
     scan_kernel(const __grid_constant__ Batch bt, const float* __restrict__ q, Ws ws) {
   extern __shared__ float smem[];
   constexpr int DPL = D / 16;  // dims per lane (half-warp per key)
-  constexpr int P = kScanKPH * G;
   const int chunk = bt.chunk;
   float* sc = smem;                        // [G][chunk] scores
   float* red = smem + G * chunk;           // [kWarps][G]
   float* thr = red + kWarps * G;           // [G]
   int* wc = reinterpret_cast<int*>(thr + G);  // [kWarps][G]
 
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();  // after the wait: see alaya_tc.cuh (attend_ovl relies on it)
   int b, h, ci;
   decode_chunk(bt, blockIdx.x, b, h, ci);
   const KSeq& s = bt.s[b];
@@ -63,19 +62,27 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
   for (int j = 0; j < G; ++j) mymax[j] = -INFINITY;
 
   const int ntiles = (valid + kScanTile - 1) / kScanTile;
-  RawFrag<T, DPL> fa[kScanKPH], fb[kScanKPH];
+  // Keys per half-warp per step: 8, or 4 when a key row is >= 32 B per lane
+  // (fp32 d=128): two register buffers of KPH rows stay at 64 registers, so
+  // the fp32 scan is not register-starved. A 128-key tile is SUB steps.
+  constexpr int KPH = (int)sizeof(T) * DPL >= 32 ? 4 : 8;
+  constexpr int SUB = kScanKPH / KPH;
+  constexpr int PK = KPH * G;
+  RawFrag<T, DPL> fa[KPH], fb[KPH];
 
-  auto load_tile = [&](int tile, RawFrag<T, DPL>(&f)[kScanKPH]) {
+  auto load_step = [&](int st, RawFrag<T, DPL>(&f)[KPH]) {
+    const int tile = st / SUB, sub = st % SUB;
 #pragma unroll
-    for (int k = 0; k < kScanKPH; ++k) {
-      int row = tile * kScanTile + hw * kScanKPH + k;
+    for (int k = 0; k < KPH; ++k) {
+      int row = tile * kScanTile + hw * kScanKPH + sub * KPH + k;
       if (row < valid) f[k].load(kb + (size_t)row * D); else f[k].zero();
     }
   };
-  auto compute_tile = [&](int tile, const RawFrag<T, DPL>(&f)[kScanKPH]) {
-    float a[P];
+  auto compute_step = [&](int st, const RawFrag<T, DPL>(&f)[KPH]) {
+    const int tile = st / SUB, sub = st % SUB;
+    float a[PK];
 #pragma unroll
-    for (int k = 0; k < kScanKPH; ++k) {
+    for (int k = 0; k < KPH; ++k) {
       float x[DPL];
       f[k].to_float(x);
 #pragma unroll
@@ -86,15 +93,29 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
         a[k * G + j] = acc;
       }
     }
-    // 8G -> 4G -> 2G -> G partials, then a plain xor over the last lane bit.
-    tr_level<8 * G>(a, 8, (hl & 8) != 0);
-    tr_level<4 * G>(a, 4, (hl & 4) != 0);
-    tr_level<2 * G>(a, 2, (hl & 2) != 0);
+    int kk;
+    bool writer;
+    if constexpr (KPH == 8) {  // 8G -> 4G -> 2G -> G partials, then xor over lane bit 0
+      tr_level<8 * G>(a, 8, (hl & 8) != 0);
+      tr_level<4 * G>(a, 4, (hl & 4) != 0);
+      tr_level<2 * G>(a, 2, (hl & 2) != 0);
 #pragma unroll
-    for (int j = 0; j < G; ++j) a[j] += __shfl_xor_sync(kFull, a[j], 1);
-    const int kk = (hl >> 1) & 7;
-    const int row = tile * kScanTile + hw * kScanKPH + kk;
-    if ((hl & 1) == 0 && row < valid) {
+      for (int j = 0; j < G; ++j) a[j] += __shfl_xor_sync(kFull, a[j], 1);
+      kk = (hl >> 1) & 7;
+      writer = (hl & 1) == 0;
+    } else {  // 4G -> 2G -> G partials, then xor over lane bits 1 and 0
+      tr_level<4 * G>(a, 8, (hl & 8) != 0);
+      tr_level<2 * G>(a, 4, (hl & 4) != 0);
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        a[j] += __shfl_xor_sync(kFull, a[j], 2);
+        a[j] += __shfl_xor_sync(kFull, a[j], 1);
+      }
+      kk = (hl >> 2) & 3;
+      writer = (hl & 3) == 0;
+    }
+    const int row = tile * kScanTile + hw * kScanKPH + sub * KPH + kk;
+    if (writer && row < valid) {
 #pragma unroll
       for (int j = 0; j < G; ++j) {
         sc[j * chunk + row] = a[j];
@@ -103,25 +124,29 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
     }
   };
 
-  // kept tiles (block filter), double-buffered: load the next while computing
+  // kept tiles (block filter), SUB steps each, double-buffered: load the next
+  // step while computing the current one
   const unsigned long long tmask = chunk_tiles(bt, ws, blockIdx.x, ntiles);
   unsigned long long mrem = tmask;
+  int tile_open = -1, sub_next = 0;
   auto pop = [&]() -> int {
+    if (tile_open >= 0 && sub_next < SUB) return tile_open * SUB + sub_next++;
     if (!mrem) return -1;
-    const int t = __ffsll((long long)mrem) - 1;
+    tile_open = __ffsll((long long)mrem) - 1;
     mrem &= mrem - 1;
-    return t;
+    sub_next = 1;
+    return tile_open * SUB;
   };
   int cur = pop();
-  if (cur >= 0) load_tile(cur, fa);
+  if (cur >= 0) load_step(cur, fa);
   while (cur >= 0) {
     const int nxt = pop();
-    if (nxt >= 0) load_tile(nxt, fb);
-    compute_tile(cur, fa);
+    if (nxt >= 0) load_step(nxt, fb);
+    compute_step(cur, fa);
     if (nxt < 0) break;
     cur = pop();
-    if (cur >= 0) load_tile(cur, fa);
-    compute_tile(nxt, fb);
+    if (cur >= 0) load_step(cur, fa);
+    compute_step(nxt, fb);
   }
 
   // chunk max per head, then the global running max (order-preserving atomic)
@@ -188,6 +213,14 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) tot += wc[w * G + j];
       publish_pair(bt, ws, cbase + j, tot);
+    }
+  }
+  if (bt.overlap) {  // chunk published: 4 units, like the tcgen05 scan's 4 epilogue warps
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      atomicAdd(&ws.group_done[b * bt.Hkv + h], 4);
+      atomicAdd(&ws.counters[6], 4);
     }
   }
 }

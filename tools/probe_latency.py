@@ -30,6 +30,7 @@ ap.add_argument("--chunk", type=int, default=0)
 ap.add_argument("--beta", type=float, default=110.0)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--locality", action="store_true")
+ap.add_argument("--fp32", action="store_true", help="fp32 K/V (CUDA-core scan)")
 ap.add_argument("--out", default=None)
 a = ap.parse_args()
 dev = torch.device("cuda")
@@ -39,14 +40,15 @@ def make(B, hkv, n, d, seed):
     g = torch.Generator(device=dev).manual_seed(seed)
     c = torch.randn(16, d, generator=g, device=dev)
     centers = c / c.norm(dim=1, keepdim=True) * math.sqrt(d)
-    K = torch.empty(B, hkv, n, d, dtype=torch.bfloat16, device=dev)
+    dt = torch.float32 if a.fp32 else torch.bfloat16
+    K = torch.empty(B, hkv, n, d, dtype=dt, device=dev)
     V = torch.empty_like(K)
     for b in range(B):
         a_ = torch.randint(0, 16, (hkv, n), generator=g, device=dev)
         if a.locality:
             a_ = torch.sort(a_, dim=1).values
-        K[b] = (centers[a_] + 0.25 * torch.randn(hkv, n, d, generator=g, device=dev)).to(torch.bfloat16)
-        V[b] = torch.randn(hkv, n, d, generator=g, device=dev).to(torch.bfloat16)
+        K[b] = (centers[a_] + 0.25 * torch.randn(hkv, n, d, generator=g, device=dev)).to(dt)
+        V[b] = torch.randn(hkv, n, d, generator=g, device=dev).to(dt)
     return K, V, centers, g
 
 
@@ -67,17 +69,17 @@ lines = []
 for B in [int(x) for x in a.batches.split(",")]:
     hkv, d = 8, 128
     K, V, centers, g = make(B, hkv, a.ctx, d, seed=B)
-    params = engine.make_params(a.hq, hkv, d, torch.bfloat16, a.beta, 16, 64, a.chunk, 0, 0)
+    params = engine.make_params(a.hq, hkv, d, K.dtype, a.beta, 16, 64, a.chunk, 0, 0)
     call = engine.Call([engine.SeqView(k=K[b], v=V[b], n=a.ctx) for b in range(B)], params,
-                       torch.bfloat16, dev)
+                       K.dtype, dev)
     pick = torch.randint(0, 16, (B, a.hq), generator=g, device=dev)
     q = (centers[pick] + 0.25 * torch.randn(B, a.hq, d, generator=g, device=dev)).float()
     out = torch.empty_like(q)
     t_full = timed(lambda: call.dipr_attention(q, out=out), a.reps)
     t_scan = timed(lambda: call.scan_only(q), a.reps)
-    kbytes = B * hkv * a.ctx * d * 2
+    kbytes = B * hkv * a.ctx * d * K.element_size()
     d_ = {"label": a.label, "B": B, "hq": a.hq, "ctx": a.ctx, "chunk": a.chunk,
-          "locality": a.locality, "us_call": round(t_full, 1), "us_scan": round(t_scan, 1),
+          "locality": a.locality, "dtype": str(K.dtype), "us_call": round(t_full, 1), "us_scan": round(t_scan, 1),
           "scan_GBps": round(kbytes / t_scan / 1e3, 1),
           "qh_per_s": round(B * a.hq / t_full * 1e6),
           "env": {k: v for k, v in os.environ.items() if k.startswith("ALAYA_")}}
