@@ -327,13 +327,6 @@ int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch
   if (!d_q || !d_out) return fail(ALAYA_ERR_ARG, "null q/out");
   for (int b = 0; b < batch; ++b)
     if (seqs[b].prefix_len + seqs[b].w == 0) return fail(ALAYA_ERR_ARG, "attention on an empty session");
-  if (c.use_tc && fused_enabled()) {  // scan + attend in one persistent kernel
-    if ((rc = c.st.prep(c.bt, d_q, c.ws, c.stream))) return rc;
-    if (c.bt.block_filter && (rc = c.st.filter(c.bt, d_q, c.ws, c.stream))) return rc;
-    c.bt.split = 0x7fffffff;  // the fused kernel runs whole (chunk, head) pairs
-    if ((rc = launch_tc_fused(c.bt, c.seqs, d_q, c.ws, c.stream))) return rc;
-    return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);
-  }
   // attend beside the scan (per-group readiness); the CUDA-core scan fills the
   // register file (no room for an attend CTA: measured no gain), so tcgen05 only
   if (c.use_tc && overlap_enabled(c.bt.B * c.bt.Hkv)) {

@@ -58,9 +58,10 @@ struct BixSet {
 struct Ws {
   int* status;
   uint32_t* gmax;   // [B*Hq] order-preserving encoded running max
-  int* counters;    // [16] right after gmax (zeroed with it): [0] attend ticket, [1] scan ticket
-                    // (fused), [2..3] block-filter kept/total, [7] overflow items
-  int* group_done;  // [B*Hkv] right after counters (zeroed with it): chunks published per group
+  int* counters;    // [16] right after gmax (zeroed by prep_kernel): [0] attend ticket,
+                    // [2..3] block-filter kept/total, [6] epilogue-warp chunk publications
+                    // (overlapped attend), [7] overflow items
+  int* group_done;  // [B*Hkv] right after counters: chunk publications per (seq, kv head)
   int* cnt;         // [chunks*G*4] candidate counts per scan sub-list (see CandList)
   int* selcnt;      // [chunks*G]
   int* retcnt;      // [chunks*G]

@@ -138,9 +138,6 @@ StageSet pick_g(int G) {
 bool tc_scan_eligible(const Batch& bt, int dtype, const alaya_seq* seqs);
 int launch_tc_scan(const Batch& bt, const alaya_seq* seqs, const float* q, const Ws& ws,
                    cudaStream_t st);
-int launch_tc_fused(const Batch& bt, const alaya_seq* seqs, const float* q, const Ws& ws,
-                    cudaStream_t st);
-bool fused_enabled();
 bool overlap_enabled(int groups);
 int64_t diprs_row_bytes(int max_n, int cap);
 int launch_diprs(const Batch& bt, int dtype, const alaya_graph* graphs, const float* q, int l0, int floor_mode,

@@ -7,7 +7,6 @@
 #include <mutex>
 
 #include "alaya_dispatch.cuh"
-#include "alaya_fused.cuh"
 #include "alaya_tc.cuh"
 
 namespace alaya {
@@ -104,21 +103,6 @@ int build_maps(const Batch& bt, const alaya_seq* seqs, tc::Maps& maps) {
   return ALAYA_OK;
 }
 
-template <int G, int S>
-int launch_fused_s(const Batch& bt, const tc::Maps& maps, const float* q, const Ws& ws, cudaStream_t st) {
-  const size_t sm = fused::fused_smem_bytes(G, S);
-  cudaFuncSetAttribute(fused::fused_tc_kernel<G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  fused::fused_tc_kernel<G, S><<<num_sms(), fused::kThreadsFused, sm, st>>>(bt, maps, q, ws, ws.group_done);
-  return cuda_check("fused_tc_kernel");
-}
-
-template <int G>
-int launch_fused(const Batch& bt, const tc::Maps& maps, const float* q, const Ws& ws, cudaStream_t st) {
-  static const int stages = env_int("ALAYA_TC_STAGES", 5);
-  if (stages <= 4) return launch_fused_s<G, 4>(bt, maps, q, ws, st);
-  return launch_fused_s<G, 5>(bt, maps, q, ws, st);
-}
-
 }  // namespace
 
 bool tc_scan_eligible(const Batch& bt, int dtype, const alaya_seq* seqs) {
@@ -145,28 +129,6 @@ bool pdl_enabled() {
 bool overlap_enabled(int groups) {
   static const int mode = env_int("ALAYA_OVERLAP", -1);
   return mode > 0 || (mode < 0 && groups >= 16);
-}
-
-bool fused_enabled() {
-  static const int on = env_int("ALAYA_FUSED", 0);
-  return on != 0;
-}
-
-int launch_tc_fused(const Batch& bt, const alaya_seq* seqs, const float* q, const Ws& ws,
-                    cudaStream_t st) {
-  static thread_local tc::Maps maps;
-  int rc = build_maps(bt, seqs, maps);
-  if (rc) return rc;
-  switch (bt.G) {
-    case 1: return launch_fused<1>(bt, maps, q, ws, st);
-    case 2: return launch_fused<2>(bt, maps, q, ws, st);
-    case 3: return launch_fused<3>(bt, maps, q, ws, st);
-    case 4: return launch_fused<4>(bt, maps, q, ws, st);
-    case 5: return launch_fused<5>(bt, maps, q, ws, st);
-    case 6: return launch_fused<6>(bt, maps, q, ws, st);
-    case 7: return launch_fused<7>(bt, maps, q, ws, st);
-    default: return launch_fused<8>(bt, maps, q, ws, st);
-  }
 }
 
 int launch_tc_scan(const Batch& bt_in, const alaya_seq* seqs, const float* q, const Ws& ws,
