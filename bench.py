@@ -467,7 +467,9 @@ def main():
                                  % (2 * K.numel() * esize / 2**30),
                            "parallelism": "seq-shard%d" % world if world > 1 else "single"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": a.steps * L * (3 if world == 1 else 4),
+                # per layer: single GPU prep, scan, attend, combine; sharded prep, scan,
+                # combine (local max), attend, combine (partial), merge
+                "gpu_launches": a.steps * L * (4 if world == 1 else 6),
                 "clocks": sampler.summary(), "parity": parity, "stats": stats,
                 "sharded_check": sharded_check,
                 "gen_seconds": round(t_gen, 2)}
