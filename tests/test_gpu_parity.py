@@ -322,3 +322,46 @@ def test_tcgen05_multi_context_batch(cuda_ok):
             o_ref, _, _ = O.head_attention_flat(q[b, qh], keys[qh // 4], vals[qh // 4], None, None,
                                                 110.0, selected_override=got)
             assert rel(out[b, qh], o_ref) <= 1e-5
+
+
+def test_overlapped_attend_path_batch(cuda_ok):
+    """>= 16 (session, kv head) groups: the default path runs the attend beside
+    the tcgen05 scan (per-group readiness counters). Ragged Llama-shaped
+    sessions with windows vs the fp64 oracle on the GPU's own selection."""
+    import paper_2504_10326_b200 as P
+    hq, hkv, d, beta = 32, 8, 128, 110.0
+    shape = P.ModelShape(1, hq, hkv, d)
+    cfg = P.EngineConfig(beta=beta, first_layers=(0,), short_context_threshold=0,
+                         kv_dtype="bfloat16")
+    db = P.ContextStore(shape, cfg)
+    r = np.random.default_rng(11)
+    sessions, data = [], []
+    for i, n in enumerate([3000, 40000, 70001]):
+        tok, keys, vals, centers, _ = O.make_context(n, 1, hkv, d, seed=70 + i)
+        keys, vals = O.bf16_round(keys), O.bf16_round(vals)
+        db.import_context(tok, keys, vals)
+        s, _ = db.create_session(tok)
+        for _ in range(i + 1):
+            kk = O.bf16_round(r.standard_normal((hkv, d)).astype(np.float32))
+            vv = O.bf16_round(r.standard_normal((hkv, d)).astype(np.float32))
+            s.update(r.standard_normal((hq, d)).astype(np.float32), kk, vv, 0)
+        sessions.append(s)
+        data.append((keys[0], vals[0], centers))
+    q = np.stack([(c[r.integers(0, 16, hq)] + 0.25 * r.standard_normal((hq, d)))
+                  for _, _, c in data]).astype(np.float32)
+    for rep in range(2):  # twice: the workspace header must be fully re-seeded per call
+        out = P.Session.attention_batch(sessions, q, 0)
+        for b, s in enumerate(sessions):
+            keys, vals, _ = data[b]
+            w = s._wlen[0]
+            wk = s._wk[0, :, :w].float().cpu().numpy()
+            wv = s._wv[0, :, :w].float().cpu().numpy()
+            ref, sels, _ = O.session_attention_flat(q[b], keys, vals, wk, wv, beta)
+            diag = s.last_diagnostics
+            for qh in range(hq):
+                h = qh // (hq // hkv)
+                got = diag["heads"][qh]["selected_base"]
+                assert boundary_ok(got, sels[qh], q[b, qh], keys[h], beta, EPS_SET["bfloat16"])
+                o_ref, _, _ = O.head_attention_flat(q[b, qh], keys[h], vals[h], wk[h], wv[h], beta,
+                                                    selected_override=got)
+                assert rel(out[b, qh], o_ref) <= 1e-5, (rep, b, qh)
