@@ -309,8 +309,25 @@ def main():
                                w=a.window_rows if kv_ring_owner else 0) for b in range(B)]
         calls.append(engine.Call(seqs, params, dtype, dev))
     out = torch.empty(L, B, Hq, d, dtype=torch.float32, device=dev)
-    from paper_2504_10326_b200.sharded import EngineStages, sharded_attention
+    from paper_2504_10326_b200.sharded import EngineStages, PeerExchange, sharded_attention
     stages = [EngineStages.from_call(c) for c in calls]
+    # sharded collectives over peer memory (NVLink P2P via CUDA IPC, alaya_exch) unless
+    # ALAYA_P2P=0; validated against the NCCL path on a real layer before use, NCCL otherwise
+    exch, collective = None, "none" if world == 1 else "nccl"
+    if world > 1 and os.environ.get("ALAYA_P2P", "1") != "0":
+        exch = PeerExchange.create(None, B * Hq * (d + 2), dev)
+        ok = exch is not None
+        if ok:
+            o_p = sharded_attention(stages[0], Q[0, 0], exchange=exch).clone()
+            o_n = sharded_attention(stages[0], Q[0, 0])
+            torch.cuda.synchronize()
+            ok = not int(exch.err.item()) and float(((o_p - o_n).norm() / o_n.norm()).item()) <= 1e-6
+        agree = torch.tensor([1 if ok else 0], device=dev if not share else "cpu")
+        dist.all_reduce(agree, op=dist.ReduceOp.MIN)
+        if int(agree.item()):
+            collective = "p2p"
+        else:
+            exch = None
 
     def step(s):
         w = a.window_rows + s + 1
@@ -322,8 +339,8 @@ def main():
                 calls[l].set_window_rows(w)
             if world == 1:
                 calls[l].dipr_attention(Q[s, l], out=out[l])
-            else:  # scan -> NCCL max-allreduce -> attend -> allgather -> merge
-                out[l].copy_(sharded_attention(stages[l], Q[s, l]))
+            else:  # scan -> max-allreduce -> attend -> allgather -> merge
+                out[l].copy_(sharded_attention(stages[l], Q[s, l], exchange=exch))
 
     for s in range(a.warmup):
         step(s)
@@ -344,6 +361,8 @@ def main():
         if world > 1:
             dist.barrier()
     ms = ev0.elapsed_time(ev1) / a.steps
+    if exch is not None and int(exch.err.item()):
+        raise SystemExit("peer exchange timed out inside the timed region: result invalid")
     if world > 1:
         t = torch.tensor([ms], device=dev if not share else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -352,7 +371,7 @@ def main():
     if world > 1 and a.check:
         # one more sharded layer-0 step vs the unsharded kernels on the full context
         s_last = a.warmup + a.steps - 1
-        o_sh = sharded_attention(stages[0], Q[s_last, 0]).clone()
+        o_sh = sharded_attention(stages[0], Q[s_last, 0], exchange=exch).clone()
         if rank == 0:
             wf = a.window_rows + a.warmup + a.steps
             full = []
@@ -465,7 +484,8 @@ def main():
                            "session_window_rows": a.window_rows, "scan_kernel": a.scan_kernel,
                            "l2": "inputs (KV %.1f GiB) >> L2 (126 MB); no flush needed"
                                  % (2 * K.numel() * esize / 2**30),
-                           "parallelism": "seq-shard%d" % world if world > 1 else "single"},
+                           "parallelism": "seq-shard%d" % world if world > 1 else "single",
+                           "collectives": collective},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 # per layer: single GPU prep, scan, attend, combine; sharded prep, scan,
                 # combine (local max), attend, combine (partial), merge

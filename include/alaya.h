@@ -252,6 +252,29 @@ int alaya_diprs(const alaya_params* p, const alaya_seq* seqs, const alaya_graph*
                 int64_t cap, int32_t* d_count, int32_t* d_explored, void* d_ws, size_t ws_bytes,
                 void* stream);
 
+/* ---- sequence-sharded exchange over peer memory -------------- */
+
+/* Bytes of one rank's symmetric exchange buffer for n_ranks ranks and
+ * messages of up to cap_floats floats (0 if out of range, n_ranks <= 16). */
+size_t alaya_exch_bytes(int n_ranks, int64_t cap_floats);
+/* cudaMalloc a zeroed exchange buffer and export its CUDA IPC handle
+ * (ipc_handle: 64 bytes, cudaIpcMemHandle_t). */
+int alaya_exch_alloc(size_t bytes, void** d_buf, void* ipc_handle);
+/* Map a peer rank's exchange buffer (cudaIpcOpenMemHandle, lazy peer access). */
+int alaya_exch_open(const void* ipc_handle, void** d_buf);
+int alaya_exch_close(void* d_buf);
+int alaya_exch_free(void* d_buf);
+/* One exchange on `stream`: bufs[r] = rank r's buffer as mapped in this process.
+ * kind 0: allreduce-max of d_local[count] into d_out (the global DIPR max,
+ * replaces ncclAllReduce(max)); kind 1: allgather of d_local[count], read the
+ * result in place at alaya_exch_slots(own buffer, ..., 1, epoch) as
+ * [n_ranks][cap_floats] (replaces ncclAllGather). epoch: 1, 2, ... per kind,
+ * the same sequence on every rank. A peer that never arrives sets *d_err. */
+int alaya_exch(void* const* bufs, int n_ranks, int rank, int64_t cap_floats, int kind,
+               const float* d_local, int64_t count, unsigned long long epoch, float* d_out, int* d_err,
+               void* stream);
+float* alaya_exch_slots(void* d_buf, int n_ranks, int64_t cap_floats, int kind, unsigned long long epoch);
+
 /* ---- AVDB vector files (reference vfs.py, docs/file-format.md) ---------- */
 
 typedef struct {

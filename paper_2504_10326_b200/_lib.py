@@ -39,6 +39,8 @@ EXPORTS = (
     "alaya_ws_candidate_counts", "alaya_topk", "alaya_block_reps", "alaya_block_topk",
     "alaya_sparse_attention", "alaya_avdb_stat", "alaya_avdb_write", "alaya_avdb_staging_bytes",
     "alaya_avdb_load", "alaya_avdb_graph", "alaya_diprs", "alaya_diprs_workspace_bytes",
+    "alaya_exch_bytes", "alaya_exch_alloc", "alaya_exch_open", "alaya_exch_close", "alaya_exch_free",
+    "alaya_exch", "alaya_exch_slots",
 )
 
 
@@ -168,6 +170,21 @@ def load() -> ctypes.CDLL:
     lib.alaya_diprs_workspace_bytes.argtypes = [P, S, G, i32]
     lib.alaya_diprs.restype = i32
     lib.alaya_diprs.argtypes = [P, S, G, i32, vp, i32, i32, vp, vp, i64, vp, vp, vp, sz, vp]
+    lib.alaya_exch_bytes.restype = sz
+    lib.alaya_exch_bytes.argtypes = [i32, i64]
+    lib.alaya_exch_alloc.restype = i32
+    lib.alaya_exch_alloc.argtypes = [sz, ctypes.POINTER(vp), vp]
+    lib.alaya_exch_open.restype = i32
+    lib.alaya_exch_open.argtypes = [vp, ctypes.POINTER(vp)]
+    lib.alaya_exch_close.restype = i32
+    lib.alaya_exch_close.argtypes = [vp]
+    lib.alaya_exch_free.restype = i32
+    lib.alaya_exch_free.argtypes = [vp]
+    lib.alaya_exch.restype = i32
+    lib.alaya_exch.argtypes = [ctypes.POINTER(vp), i32, i32, i64, i32, vp, i64, ctypes.c_uint64, vp, vp,
+                               vp]
+    lib.alaya_exch_slots.restype = vp
+    lib.alaya_exch_slots.argtypes = [vp, i32, i64, i32, ctypes.c_uint64]
     lib.alaya_ws_status.restype = vp
     lib.alaya_ws_status.argtypes = [vp]
     _lib = lib

@@ -24,6 +24,7 @@ CPU (gloo) tests can drive it with a host double; the product path passes
 
 from __future__ import annotations
 
+import ctypes
 from typing import Protocol
 
 import torch
@@ -78,9 +79,111 @@ def _staged(t: torch.Tensor, group) -> tuple[torch.Tensor, bool]:
     return t, False
 
 
-def sharded_attention(stages: LocalStages, q: torch.Tensor, group=None) -> torch.Tensor:
+class PeerExchange:
+    """The two collectives over peer memory instead of NCCL (``alaya_exch``):
+    every rank owns one symmetric device buffer, exports its CUDA IPC handle,
+    maps every peer's buffer (NVLink P2P) and exchanges by direct stores plus
+    release/acquire epoch flags. Messages up to ``cap`` floats. Build it
+    collectively on every rank of ``group``; ``None`` from :meth:`create` means
+    peer mapping is unavailable (the caller keeps NCCL)."""
+
+    def __init__(self, bufs: list[int], own: int, rank: int, world: int, cap: int,
+                 device: torch.device, opened: list[int]):
+        self.bufs, self.own, self.rank, self.world, self.cap = bufs, own, rank, world, cap
+        self.device = device
+        self._opened = opened
+        self.epoch = [0, 0]
+        self.err = torch.zeros(1, dtype=torch.int32, device=device)
+        self._arr = (ctypes.c_void_p * world)(*bufs)
+
+    @classmethod
+    def create(cls, group, cap: int, device: torch.device) -> "PeerExchange | None":
+        from . import _lib
+        lib = _lib.load()
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        nbytes = lib.alaya_exch_bytes(world, cap)
+        ok, own, handle = False, ctypes.c_void_p(), (ctypes.c_char * 64)()
+        if nbytes:
+            with torch.cuda.device(device):
+                ok = lib.alaya_exch_alloc(nbytes, ctypes.byref(own), handle) == 0
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(handle) if ok else None, group=group)
+        if not all(h is not None for h in handles):
+            return None
+        bufs, opened, good = [], [], True
+        with torch.cuda.device(device):
+            for r, h in enumerate(handles):
+                if r == rank:
+                    bufs.append(own.value)
+                    continue
+                ptr = ctypes.c_void_p()
+                hb = (ctypes.c_char * 64).from_buffer_copy(h)
+                if lib.alaya_exch_open(hb, ctypes.byref(ptr)) != 0:
+                    good = False
+                    break
+                bufs.append(ptr.value)
+                opened.append(ptr.value)
+        flags = [None] * world
+        dist.all_gather_object(flags, good, group=group)
+        if not all(flags):
+            return None
+        dist.barrier(group=group)
+        return cls(bufs, own.value, rank, world, cap, device, opened)
+
+    def _run(self, kind: int, local: torch.Tensor, out: torch.Tensor | None) -> int:
+        from . import _lib
+        local = local.to(torch.float32).contiguous()
+        if local.numel() > self.cap:
+            raise ValueError(f"exchange of {local.numel()} floats > cap {self.cap}")
+        self.epoch[kind] += 1
+        e = self.epoch[kind]
+        _lib.check(_lib.load().alaya_exch(self._arr, self.world, self.rank, self.cap, kind,
+                                          local.data_ptr(), local.numel(), e,
+                                          out.data_ptr() if out is not None else None,
+                                          self.err.data_ptr(),
+                                          torch.cuda.current_stream(self.device).cuda_stream))
+        self._keep = local
+        return e
+
+    def allreduce_max(self, local: torch.Tensor) -> torch.Tensor:
+        out = torch.empty_like(local, dtype=torch.float32)
+        self._run(0, local, out)
+        return out.view(local.shape)
+
+    def allgather(self, local: torch.Tensor) -> torch.Tensor:
+        """``[world, *local.shape]`` view of this rank's slots (valid until the
+        exchange after next of this kind)."""
+        from . import _lib
+        e = self._run(1, local, None)
+        ptr = _lib.load().alaya_exch_slots(self.own, self.world, self.cap, 1, e)
+        n = local.numel()
+        flat = _tensor_at(ptr, self.world * self.cap, self.device)
+        return flat.view(self.world, self.cap)[:, :n].reshape((self.world,) + tuple(local.shape))
+
+    def check(self) -> None:
+        if int(self.err.item()):
+            raise RuntimeError("peer exchange timed out: a rank never arrived")
+
+
+def _tensor_at(ptr: int, numel: int, device: torch.device) -> torch.Tensor:
+    """A float32 tensor over existing device memory (no copy, not owned)."""
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (numel,), "typestr": "<f4", "data": (ptr, False),
+                                    "version": 3, "strides": None}
+    return torch.as_tensor(_Arr(), device=device)
+
+
+def sharded_attention(stages: LocalStages, q: torch.Tensor, group=None,
+                      exchange: PeerExchange | None = None) -> torch.Tensor:
     """One decode step of one layer over sequence-sharded KV -> ``[B, Hq, d]``
-    (identical on every rank)."""
+    (identical on every rank). With ``exchange`` the two collectives run over
+    peer memory (``alaya_exch``), otherwise through ``torch.distributed``."""
+    if exchange is not None:
+        smax = exchange.allreduce_max(stages.scan(q))
+        part = stages.attend(q, smax).contiguous()
+        parts = exchange.allgather(part)
+        out = stages.merge(parts)
+        return out.view(q.shape[0], q.shape[1], -1)
     world = dist.get_world_size(group)
     smax = stages.scan(q)
     sm, moved = _staged(smax, group)

@@ -19,7 +19,7 @@ HEADER = ROOT / "include" / "alaya.h"
 
 def test_library_exports_every_declared_symbol():
     lib = _lib.load()
-    declared = set(re.findall(r"^\s*(?:int|size_t|const char\*|int\*)\s+(alaya_\w+)\(",
+    declared = set(re.findall(r"^\s*(?:int|size_t|const char\*|int\*|float\*)\s+(alaya_\w+)\(",
                               HEADER.read_text(), re.M))
     assert declared == set(_lib.EXPORTS)
     for name in declared:

@@ -75,3 +75,92 @@ def test_shard_emulation_matches_unsharded(cuda_ok, kv, world):
             assert len(set(sel_sh[b][qh]) ^ set(sels[qh].tolist())) <= 1
             assert rel(o_sh[b, qh], ref[qh]) <= 1e-5 + (1e-5 if kv == "bfloat16" else 0)
             assert rel(o_sh[b, qh], o_full[b, qh]) <= 2e-6
+
+
+def _exchange_group(world, cap, dev):
+    """`world` emulated ranks in ONE process: each owns an exchange buffer and
+    sees all of them as its peers (the IPC mapping step is the only part a
+    multi-process run adds). Each rank's kernels go on its own stream."""
+    import ctypes
+
+    from paper_2504_10326_b200 import _lib
+    from paper_2504_10326_b200.sharded import PeerExchange
+    lib = _lib.load()
+    bufs = []
+    for _ in range(world):
+        own, h = ctypes.c_void_p(), (ctypes.c_char * 64)()
+        assert lib.alaya_exch_alloc(lib.alaya_exch_bytes(world, cap), ctypes.byref(own), h) == 0
+        bufs.append(own.value)
+    return [PeerExchange(bufs, bufs[r], r, world, cap, dev, []) for r in range(world)], bufs
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_peer_exchange_collectives(cuda_ok, world):
+    dev = torch.device("cuda")
+    rows, d = 64, 128
+    cap = rows * (d + 2)
+    exs, bufs = _exchange_group(world, cap, dev)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    g = torch.Generator(device=dev).manual_seed(world)
+    for step in range(5):  # epochs 1..5 on both kinds (slot parity alternates)
+        loc = [torch.randn(rows, generator=g, device=dev) for _ in range(world)]
+        parts = [torch.randn(rows, d + 2, generator=g, device=dev) for _ in range(world)]
+        torch.cuda.synchronize()
+        mx, gathered = [None] * world, [None] * world
+        for r in range(world):  # launches return at once: the ranks' kernels run concurrently
+            with torch.cuda.stream(streams[r]):
+                mx[r] = exs[r].allreduce_max(loc[r])
+                gathered[r] = exs[r].allgather(parts[r]).clone()
+        torch.cuda.synchronize()
+        want = torch.stack(loc).amax(0)
+        for r in range(world):
+            exs[r].check()
+            assert torch.equal(mx[r], want)
+            assert torch.equal(gathered[r], torch.stack(parts))
+    from paper_2504_10326_b200 import _lib
+    for b in bufs:
+        _lib.load().alaya_exch_free(b)
+
+
+def test_sharded_attention_over_peer_exchange(cuda_ok):
+    """The full sharded step with the peer-memory collectives (ranks emulated on
+    streams of one GPU) equals the unsharded kernels."""
+    from paper_2504_10326_b200 import engine
+    from paper_2504_10326_b200.sharded import EngineStages, local_view, sharded_attention
+    dev = torch.device("cuda")
+    world, B, hkv, g, d, n, w, beta = 3, 2, 2, 4, 128, 30000, 2, 110.0
+    dtype = torch.bfloat16
+    r = np.random.default_rng(5)
+    K, V, WK, WV, qs = [], [], [], [], []
+    for b in range(B):
+        _, k, v, centers, _ = O.make_context(n, 1, hkv, d, seed=300 + b)
+        K.append(torch.from_numpy(O.bf16_round(k)[0]).to(dev, dtype))
+        V.append(torch.from_numpy(O.bf16_round(v)[0]).to(dev, dtype))
+        WK.append(torch.randn(hkv, w, d, device=dev).to(dtype))
+        WV.append(torch.randn(hkv, w, d, device=dev).to(dtype))
+        qs.append(centers[r.integers(0, 16, hkv * g)] + 0.25 * r.standard_normal((hkv * g, d)))
+    q = torch.tensor(np.stack(qs), dtype=torch.float32, device=dev)
+    params = engine.make_params(hkv * g, hkv, d, dtype, beta, 16, 64)
+    full = engine.Call([engine.SeqView(k=K[b], v=V[b], n=n, wk=WK[b], wv=WV[b], w=w)
+                        for b in range(B)], params, dtype, dev,
+                       ws=torch.empty(1, dtype=torch.uint8, device=dev))
+    o_full = full.dipr_attention(q).clone()
+    stages = [EngineStages([local_view(K[b], V[b], world, rk, WK[b], WV[b], w) for b in range(B)],
+                           params, dtype, dev) for rk in range(world)]
+    for st in stages:
+        st.call.ws = torch.empty(st.call.ws_bytes, dtype=torch.uint8, device=dev)
+    exs, bufs = _exchange_group(world, B * hkv * g * (d + 2), dev)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    torch.cuda.synchronize()
+    for _ in range(3):
+        outs = [None] * world
+        for rk in range(world):
+            with torch.cuda.stream(streams[rk]):
+                outs[rk] = sharded_attention(stages[rk], q, exchange=exs[rk])
+        torch.cuda.synchronize()
+        for rk in range(world):
+            exs[rk].check()
+            assert float(((outs[rk] - o_full).norm() / o_full.norm()).item()) <= 2e-6
+    from paper_2504_10326_b200 import _lib
+    for b in bufs:
+        _lib.load().alaya_exch_free(b)
