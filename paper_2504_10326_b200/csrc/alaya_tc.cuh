@@ -307,14 +307,12 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 4 : (kStages <= 3 
   const int chunk = bt.chunk;
   // The TMA producer streams K (context memory, untouched by the preceding
   // kernels) without waiting for them, so the first tiles are in flight while
-  // prep_kernel still runs. Every other warp waits (q, gmax seeds, tickets),
-  // then triggers: a dependent launched after the trigger sees all earlier
-  // work complete. (With the block filter the preceding kernel is a plain
-  // launch that never triggers, so this grid starts after it completes.)
-  if (warp != 0) {
-    pdl_wait();
-    pdl_trigger();
-  }
+  // prep_kernel still runs -- unless the block filter's keep masks (written by
+  // the preceding kernels) steer it. Every other warp waits (q, gmax seeds,
+  // tickets), then triggers: a dependent launched after the trigger sees all
+  // earlier work complete.
+  if (warp != 0 || bt.block_filter) pdl_wait();
+  if (warp != 0) pdl_trigger();
 
   if (warp == 0) {
     // ===================== TMA producer =====================
