@@ -300,6 +300,12 @@ def main():
     t_gen = time.perf_counter() - t_gen
 
     kv_ring_owner = last_rank  # session-window rows live on the last shard
+    # Session.update per layer = one alaya_window_append for all sessions (fp32 in, the
+    # rows are bf16-exact, so the ring holds the same values as a direct bf16 copy)
+    KNf, VNf = KN.float(), VN.float()
+    append_params = engine.make_params(Hq, Hkv, d, dtype, 0.0, 0, 0)
+    append_seqs = [[engine.SeqView(k=None, v=None, n=0, wk=WK[l, b], wv=WV[l, b], w=0)
+                    for b in range(B)] for l in range(L)]
     params = engine.make_params(Hq, Hkv, d, dtype, a.beta, 16, 64, 0,
                                 {"auto": 0, "cuda_core": 1, "tcgen05": 2}[a.scan_kernel])
     calls = []
@@ -333,8 +339,9 @@ def main():
         w = a.window_rows + s + 1
         for l in range(L):
             if kv_ring_owner or a.check:  # Session.update: append this token's K/V
-                WK[l, :, :, w - 1] = KN[s, l]  # (--check: every rank mirrors the ring so
-                WV[l, :, :, w - 1] = VN[s, l]  # rank 0 can run the unsharded reference)
+                for sv in append_seqs[l]:   # (--check: every rank mirrors the ring so
+                    sv.w = w - 1            # rank 0 can run the unsharded reference)
+                engine.window_append(append_seqs[l], append_params, dtype, KNf[s, l], VNf[s, l])
             if kv_ring_owner:
                 calls[l].set_window_rows(w)
             if world == 1:
@@ -487,9 +494,11 @@ def main():
                            "parallelism": "seq-shard%d" % world if world > 1 else "single",
                            "collectives": collective},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                # per layer: single GPU prep, scan, attend, combine; sharded prep, scan,
-                # combine (local max), attend, combine (partial), merge
-                "gpu_launches": a.steps * L * (4 if world == 1 else 6),
+                # per layer: window append + (single GPU) prep, scan, attend, combine, or
+                # (sharded) prep, scan, combine (local max), attend, combine (partial), merge
+                # + 2 exchanges (peer path; NCCL's own kernels not counted)
+                "gpu_launches": a.steps * L * (5 if world == 1 else
+                                               (9 if collective == "p2p" else 7)),
                 "clocks": sampler.summary(), "parity": parity, "stats": stats,
                 "sharded_check": sharded_check,
                 "gen_seconds": round(t_gen, 2)}
