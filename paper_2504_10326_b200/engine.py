@@ -364,12 +364,8 @@ def merge_states(parts: torch.Tensor, dim: int) -> torch.Tensor:
     return out
 
 
-def window_append(seqs: list[SeqView], params: AlayaParams, dtype: torch.dtype,
-                  k: torch.Tensor, v: torch.Tensor) -> None:
-    """Append ``k``/``v`` ``[B, Hkv, d]`` (fp32) as row ``seqs[b].w`` of each
-    sequence's window ring (``Session.update``, reference ``store.py:179-181``)."""
-    require_cuda()
-    lib = _lib.load()
+def append_array(seqs: list[SeqView], params: AlayaParams, dtype: torch.dtype):
+    """Validated ``alaya_seq`` descriptors of window rings for ``window_append_raw``."""
     arr = (AlayaSeq * len(seqs))()
     for i, s in enumerate(seqs):
         _check_kv(s.wk, "wk", dtype, params.dim)
@@ -377,10 +373,23 @@ def window_append(seqs: list[SeqView], params: AlayaParams, dtype: torch.dtype,
         e = arr[i]
         e.wk, e.wv, e.w_head_stride = s.wk.data_ptr(), s.wv.data_ptr(), s.wk.stride(0)
         e.w = int(s.w)
+    return arr
+
+
+def window_append_raw(arr, n: int, params: AlayaParams, k: torch.Tensor, v: torch.Tensor) -> None:
+    lib = _lib.load()
     k = k.to(torch.float32).contiguous()
     v = v.to(torch.float32).contiguous()
-    check(lib.alaya_window_append(ctypes.byref(params), arr, len(seqs), k.data_ptr(), v.data_ptr(),
+    check(lib.alaya_window_append(ctypes.byref(params), arr, n, k.data_ptr(), v.data_ptr(),
                                   torch.cuda.current_stream(k.device).cuda_stream))
+
+
+def window_append(seqs: list[SeqView], params: AlayaParams, dtype: torch.dtype,
+                  k: torch.Tensor, v: torch.Tensor) -> None:
+    """Append ``k``/``v`` ``[B, Hkv, d]`` (fp32) as row ``seqs[b].w`` of each
+    sequence's window ring (``Session.update``, reference ``store.py:179-181``)."""
+    require_cuda()
+    window_append_raw(append_array(seqs, params, dtype), len(seqs), params, k, v)
 
 
 def block_bounds(k: torch.Tensor) -> torch.Tensor:

@@ -30,7 +30,8 @@ import torch
 from . import _lib, engine, vfs
 from .config import EngineConfig
 from .core import ModelShape, WindowConfig
-from .planner import IndexKind, Plan, PlanRequest, QueryKind, plan as make_plan
+from .planner import (IndexKind, Plan, PlanRequest, QueryKind, coarse_residency_bytes,
+                      plan as make_plan)
 
 _TORCH_DTYPE = {"float32": torch.float32, "bfloat16": torch.bfloat16}
 _SCAN_KIND = {"auto": _lib.SCAN_AUTO, "cuda_core": _lib.SCAN_CUDA_CORE,
@@ -184,17 +185,14 @@ class Session:
                              f"{tuple(q.shape)}")
         if tuple(k.shape) != (B, shape.n_kv_heads, shape.dim) or tuple(v.shape) != tuple(k.shape):
             raise ValueError(f"k/v must be {(shape.n_kv_heads, shape.dim)} per session")
-        seqs = []
         for s in sessions:
             if s._store is not st:
                 raise ValueError("all sessions of a batch must share a store")
             s._check_layer(layer)
             s._ensure_window(s._wlen[layer] + 1)
-            seqs.append(engine.SeqView(k=None, v=None, n=0, wk=s._wk[layer], wv=s._wv[layer],
-                                       w=s._wlen[layer]))
         kd = _to_device(k, st.device, torch.float32)
         vd = _to_device(v, st.device, torch.float32)
-        engine.window_append(seqs, st._append_params(), st.kv_dtype, kd, vd)
+        st._append(sessions, layer, kd, vd)
         for b, s in enumerate(sessions):
             s._wlen[layer] += 1
             if st.log_queries:
@@ -352,6 +350,13 @@ class Session:
             return e, e
         return self.base.keys[layer, head, :p], self.base.values[layer, head, :p]
 
+    def _view_sig(self, layer: int) -> tuple:
+        """Identity of what _seq_view would describe, without building tensors."""
+        p = self.reused_prefix_len if self.base is not None else 0
+        w = self._wlen[layer]
+        return (id(self.base) if p else 0, p, id(self._wk) if w else 0,
+                bool(p and self._store.config.block_filter))
+
     def _seq_view(self, layer: int) -> engine.SeqView:
         p = self.reused_prefix_len if self.base is not None else 0
         w = self._wlen[layer]
@@ -390,10 +395,25 @@ class Session:
             return self.plan_override
         partial = (self.base is not None and 0 < self.reused_prefix_len < self.base.length
                    and self.reused_prefix_len < self.total_len)
-        req = PlanRequest(context_len=self.total_len, layer=layer, shape=self._store.shape,
-                          memory_budget_bytes=self._store.config.memory_budget_bytes,
+        st = self._store
+        cfg = st.config
+        n = self.total_len
+        # the planner's decision depends on n only through these comparisons
+        # (planner.py:99-120), so plans are memoised per decision key
+        key = (layer, n <= cfg.short_context_threshold,
+               self.reused_prefix_len if partial else None,
+               cfg.memory_budget_bytes >= coarse_residency_bytes(n, st.shape.dim, cfg.resident_fraction))
+        hit = st._plan_cache.get(key)
+        if hit is not None:
+            return hit
+        req = PlanRequest(context_len=n, layer=layer, shape=st.shape,
+                          memory_budget_bytes=cfg.memory_budget_bytes,
                           reused_prefix_len=self.reused_prefix_len if partial else None)
-        return make_plan(req, self._store.config.planner_config())
+        plan = make_plan(req, st._planner_cfg)
+        if len(st._plan_cache) > 65536:
+            st._plan_cache.clear()
+        st._plan_cache[key] = plan
+        return plan
 
     def full_kv(self, layer: int, head: int):
         bk, bv = self._base_arrays(layer, head)
@@ -419,6 +439,8 @@ class ContextStore:
         self.log_queries = log_queries
         self.contexts: dict[str, ContextRecord] = {}
         self._calls: dict = {}
+        self._plan_cache: dict = {}
+        self._planner_cfg = self.config.planner_config()
         self.root = Path(root) if root is not None else None
         self.pool = None
         if self.root is not None:
@@ -592,24 +614,45 @@ class ContextStore:
                                          for l in range(self.shape.n_layers)])
         return record.bounds
 
+    def _append(self, sessions: list["Session"], layer: int, kd: torch.Tensor, vd: torch.Tensor):
+        """One alaya_window_append for the batch; descriptors cached per (layer,
+        sessions) and rebuilt only when a window ring was reallocated."""
+        sig = tuple(id(s._wk) for s in sessions)
+        key = ("append", layer, tuple(id(s) for s in sessions))
+        hit = self._calls.get(key)
+        if hit is None or hit[0] != sig:
+            seqs = [engine.SeqView(k=None, v=None, n=0, wk=s._wk[layer], wv=s._wv[layer], w=0)
+                    for s in sessions]
+            arr = engine.append_array(seqs, self._append_params(), self.kv_dtype)
+            hit = (sig, arr, [s._wk for s in sessions] + [s._wv for s in sessions])
+            if len(self._calls) > 4096:
+                self._calls.clear()
+            self._calls[key] = hit
+        arr = hit[1]
+        for i, s in enumerate(sessions):
+            arr[i].w = s._wlen[layer]
+        engine.window_append_raw(arr, len(sessions), self._append_params(), kd, vd)
+
     def _append_params(self):
-        sh = self.shape
-        return engine.make_params(sh.n_query_heads, sh.n_kv_heads, sh.dim, self.kv_dtype, 0.0, 0, 0)
+        ap = getattr(self, "_ap", None)
+        if ap is None:
+            sh = self.shape
+            ap = self._ap = engine.make_params(sh.n_query_heads, sh.n_kv_heads, sh.dim,
+                                               self.kv_dtype, 0.0, 0, 0)
+        return ap
 
     def _call_for(self, sessions: list["Session"], layer: int, beta: float, wi: int, wl: int):
         """Validated C-ABI descriptors for (layer, sessions), cached across steps:
         only the window row counts change between decode steps."""
-        views = [s._seq_view(layer) for s in sessions]
-        sig = tuple((v.k.data_ptr() if v.k is not None else 0, v.n,
-                     v.wk.data_ptr() if v.wk is not None else 0,
-                     v.bounds.data_ptr() if v.bounds is not None else 0) for v in views)
+        sig = tuple(s._view_sig(layer) for s in sessions)
         key = (layer, tuple(id(s) for s in sessions), beta, wi, wl)
         hit = self._calls.get(key)
-        if hit is not None and hit[0] == sig:
+        if hit is not None and hit[0] == sig:  # (the entry holds the objects the ids name)
             call = hit[1]
-            for i, v in enumerate(views):
-                call.seqs[i].w = int(v.w)
+            for i, s in enumerate(sessions):
+                call.seqs[i].w = s._wlen[layer]
             return call
+        views = [s._seq_view(layer) for s in sessions]
         sh = self.shape
         params = engine.make_params(sh.n_query_heads, sh.n_kv_heads, sh.dim, self.kv_dtype, beta,
                                     wi, wl, self.config.chunk, _SCAN_KIND[self.config.scan_kernel],
@@ -617,7 +660,8 @@ class ContextStore:
         call = engine.Call(views, params, self.kv_dtype, self.device)
         if len(self._calls) > 4096:
             self._calls.clear()
-        self._calls[key] = (sig, call)
+        # strong references keep the ids in `sig` from being reused by new objects
+        self._calls[key] = (sig, call, [(s.base, s._wk) for s in sessions])
         return call
 
     def _plans_for(self, n: int) -> dict[int, Plan]:
