@@ -314,9 +314,10 @@ int alaya_window_append(const alaya_params* p, const alaya_seq* seqs, int batch,
   const long total = (long)batch * p->n_kv_heads * p->dim;
   const int blocks = (int)std::min<long>((total + 255) / 256, 1024);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (p->dtype == ALAYA_BF16) window_append_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(bt, d_k, d_v);
-  else window_append_kernel<float><<<blocks, 256, 0, st>>>(bt, d_k, d_v);
-  return cuda_check("window_append_kernel");
+  if (p->dtype == ALAYA_BF16)
+    return launch_pdl("window_append_kernel", window_append_kernel<__nv_bfloat16>, blocks, 256, 0, st, bt, d_k,
+                      d_v);
+  return launch_pdl("window_append_kernel", window_append_kernel<float>, blocks, 256, 0, st, bt, d_k, d_v);
 }
 
 int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q,

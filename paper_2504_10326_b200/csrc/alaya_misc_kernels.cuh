@@ -66,6 +66,8 @@ __global__ void selected_kernel(const __grid_constant__ Batch bt, Ws ws, int64_t
 template <typename T>
 __global__ void window_append_kernel(const __grid_constant__ Batch bt, const float* __restrict__ k,
                                      const float* __restrict__ v) {
+  pdl_wait();  // PDL launch: the previous layer's kernels may still be finishing
+  pdl_trigger();
   const int D = bt.D;
   const long total = (long)bt.B * bt.Hkv * D;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
