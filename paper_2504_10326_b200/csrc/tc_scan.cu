@@ -124,11 +124,11 @@ bool pdl_enabled() {
 }
 
 // attend beside the scan: ALAYA_OVERLAP=0 off, 1 on, default (-1) on when the
-// call has >= 16 (sequence, kv head) groups (measured: +8% at 4-8 sessions of
-// 128K, slightly slower at 1 session where the scan tail is short)
+// call has >= 32 (sequence, kv head) groups (measured at 128K: +8% at 4-8
+// sessions of 8 kv heads, neutral to -1% at 1-2 sessions)
 bool overlap_enabled(int groups) {
   static const int mode = env_int("ALAYA_OVERLAP", -1);
-  return mode > 0 || (mode < 0 && groups >= 16);
+  return mode > 0 || (mode < 0 && groups >= 32);
 }
 
 int launch_tc_scan(const Batch& bt_in, const alaya_seq* seqs, const float* q, const Ws& ws,

@@ -325,7 +325,7 @@ def test_tcgen05_multi_context_batch(cuda_ok):
 
 
 def test_overlapped_attend_path_batch(cuda_ok):
-    """>= 16 (session, kv head) groups: the default path runs the attend beside
+    """>= 32 (session, kv head) groups: the default path runs the attend beside
     the tcgen05 scan (per-group readiness counters). Ragged Llama-shaped
     sessions with windows vs the fp64 oracle on the GPU's own selection."""
     import paper_2504_10326_b200 as P
@@ -336,7 +336,7 @@ def test_overlapped_attend_path_batch(cuda_ok):
     db = P.ContextStore(shape, cfg)
     r = np.random.default_rng(11)
     sessions, data = [], []
-    for i, n in enumerate([3000, 40000, 70001]):
+    for i, n in enumerate([3000, 40000, 70001, 5000]):
         tok, keys, vals, centers, _ = O.make_context(n, 1, hkv, d, seed=70 + i)
         keys, vals = O.bf16_round(keys), O.bf16_round(vals)
         db.import_context(tok, keys, vals)
