@@ -29,9 +29,9 @@ struct Peers {
   char* p[kMaxPeers];
 };
 
-// symmetric buffer: [2 kinds][kMaxPeers] u64 flags, then slots:
-// [parity 2][kind 2][R][cap] floats
-constexpr size_t kFlagBytes = 2 * kMaxPeers * 8;
+// symmetric buffer: [2 kinds][kMaxPeers] u64 flags + an arrival counter (u64
+// slot), padded to 512 B, then slots: [parity 2][kind 2][R][cap] floats
+constexpr size_t kFlagBytes = 512;
 
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -45,6 +45,57 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 __device__ __forceinline__ float* slot(char* buf, int parity, int kind, int r, int R, int64_t cap) {
   float* base = reinterpret_cast<float*>(buf + kFlagBytes);
   return base + ((((size_t)parity * 2 + kind) * R + r) * (size_t)cap);
+}
+
+// Allgather of larger messages (e.g. 0.5 MB of partial states per rank at 32
+// sessions): several CTAs push disjoint segments to every peer; the last CTA to
+// finish (arrival counter in the own buffer, after the flags) raises the flags;
+// CTA 0 then waits for all R flags, so the kernel ends when every rank's data
+// has landed here. All CTAs are co-resident (grid <= 64).
+__global__ void __launch_bounds__(kExThreads)
+    exch_gather_kernel(const float* __restrict__ local, int64_t count, int64_t cap,
+                       __grid_constant__ const Peers peers, int rank, int R, unsigned long long epoch,
+                       int* __restrict__ err) {
+  const int parity = (int)(epoch & 1ull);
+  const int64_t seg = (count + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * seg, hi = min(count, lo + seg);
+  for (int p = 0; p < R; ++p) {
+    float* dst = slot(peers.p[p], parity, 1, rank, R, cap);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) dst[i] = local[i];
+  }
+  __threadfence_system();
+  __syncthreads();
+  __shared__ int s_last;
+  unsigned int* arrive = reinterpret_cast<unsigned int*>(
+      reinterpret_cast<unsigned long long*>(peers.p[rank]) + 2 * kMaxPeers);  // own counter
+  if (threadIdx.x == 0) s_last = atomicAdd(arrive, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last) {
+    if (threadIdx.x == 0) *arrive = 0u;  // next exchange starts after this kernel
+    __threadfence_system();
+    if (threadIdx.x < R) {
+      unsigned long long* f = reinterpret_cast<unsigned long long*>(peers.p[threadIdx.x]) + kMaxPeers + rank;
+      st_release_sys(f, epoch);
+    }
+  }
+  if (blockIdx.x != 0) return;
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  if (threadIdx.x < R) {
+    const unsigned long long* f =
+        reinterpret_cast<const unsigned long long*>(peers.p[rank]) + kMaxPeers + threadIdx.x;
+    long long polls = 0;
+    while (ld_acquire_sys(f) < epoch) {
+      if (++polls > (1ll << 26)) {
+        atomicExch(&s_bad, 1);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  if (s_bad && threadIdx.x == 0 && err) atomicExch(err, 1);
 }
 
 // kind 0: allreduce-max of `count` floats into out; kind 1: allgather (out unused:
@@ -147,8 +198,15 @@ int alaya_exch(void* const* bufs, int n_ranks, int rank, int64_t cap_floats, int
   if (epoch == 0) return fail(ALAYA_ERR_ARG, "epochs start at 1");
   Peers pp;
   for (int r = 0; r < kMaxPeers; ++r) pp.p[r] = r < n_ranks ? static_cast<char*>(bufs[r]) : nullptr;
-  exch_kernel<<<1, kExThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      d_local, count, cap_floats, pp, rank, n_ranks, epoch, kind, d_out, d_err);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (kind == 1) {
+    const int grid = (int)std::min<int64_t>(64, std::max<int64_t>(1, (count + 8191) / 8192));
+    exch_gather_kernel<<<grid, kExThreads, 0, st>>>(d_local, count, cap_floats, pp, rank, n_ranks, epoch,
+                                                    d_err);
+    return cuda_check("exch_gather_kernel");
+  }
+  exch_kernel<<<1, kExThreads, 0, st>>>(d_local, count, cap_floats, pp, rank, n_ranks, epoch, kind, d_out,
+                                        d_err);
   return cuda_check("exch_kernel");
 }
 

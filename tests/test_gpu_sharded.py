@@ -107,9 +107,15 @@ def test_peer_exchange_collectives(cuda_ok, world):
         parts = [torch.randn(rows, d + 2, generator=g, device=dev) for _ in range(world)]
         torch.cuda.synchronize()
         mx, gathered = [None] * world, [None] * world
-        for r in range(world):  # launches return at once: the ranks' kernels run concurrently
+        # launches return at once, so the ranks' kernels run concurrently. Emulated ranks
+        # share one GPU's launch queues, so each exchange is issued for every rank before
+        # the next one (issuing rank by rank can leave a rank's exchange queued behind
+        # another rank's spinning kernel; one process per GPU has no such coupling)
+        for r in range(world):
             with torch.cuda.stream(streams[r]):
                 mx[r] = exs[r].allreduce_max(loc[r])
+        for r in range(world):
+            with torch.cuda.stream(streams[r]):
                 gathered[r] = exs[r].allgather(parts[r]).clone()
         torch.cuda.synchronize()
         want = torch.stack(loc).amax(0)
@@ -126,7 +132,7 @@ def test_sharded_attention_over_peer_exchange(cuda_ok):
     """The full sharded step with the peer-memory collectives (ranks emulated on
     streams of one GPU) equals the unsharded kernels."""
     from paper_2504_10326_b200 import engine
-    from paper_2504_10326_b200.sharded import EngineStages, local_view, sharded_attention
+    from paper_2504_10326_b200.sharded import EngineStages, local_view
     dev = torch.device("cuda")
     world, B, hkv, g, d, n, w, beta = 3, 2, 2, 4, 128, 30000, 2, 110.0
     dtype = torch.bfloat16
@@ -153,10 +159,19 @@ def test_sharded_attention_over_peer_exchange(cuda_ok):
     streams = [torch.cuda.Stream() for _ in range(world)]
     torch.cuda.synchronize()
     for _ in range(3):
-        outs = [None] * world
+        # sharded_attention's exchange branch, phase by phase across the emulated ranks
+        # (see test_peer_exchange_collectives for why); bench.py --check with
+        # ALAYA_BENCH_SHARE_GPU=1 runs the branch itself in separate processes
+        smax, parts, outs = [None] * world, [None] * world, [None] * world
         for rk in range(world):
             with torch.cuda.stream(streams[rk]):
-                outs[rk] = sharded_attention(stages[rk], q, exchange=exs[rk])
+                smax[rk] = exs[rk].allreduce_max(stages[rk].scan(q))
+        for rk in range(world):
+            with torch.cuda.stream(streams[rk]):
+                parts[rk] = exs[rk].allgather(stages[rk].attend(q, smax[rk]).contiguous())
+        for rk in range(world):
+            with torch.cuda.stream(streams[rk]):
+                outs[rk] = stages[rk].merge(parts[rk]).view(q.shape[0], q.shape[1], -1)
         torch.cuda.synchronize()
         for rk in range(world):
             exs[rk].check()
