@@ -136,7 +136,7 @@ size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 struct Layout {
   size_t zero_bytes;
   size_t status, gmax, counters, cnt, selcnt, retcnt, part_l, part_acc, cidx, cscore, partbuf, smaxbuf,
-      keep, lbu, ovl_l, ovl_acc, ovl_sel, ovl_ret, heavy, ovlist, total;
+      keep, ovl_l, ovl_acc, ovl_sel, ovl_ret, heavy, ovlist, total;
 };
 
 Layout layout_for(const Batch& bt) {
@@ -145,8 +145,7 @@ Layout layout_for(const Batch& bt) {
   size_t o = 0;
   L.status = o; o = align_up(o + 4);
   L.gmax = o; L.counters = o + 4 * rows;
-  L.lbu = L.counters + 64 + 4 * (size_t)bt.B * bt.Hkv;
-  L.zero_bytes = 4 * rows + 64 + 4 * (size_t)bt.B * bt.Hkv + 4 * rows;  // gmax, counters, group_done, lbu
+  L.zero_bytes = 4 * rows + 64 + 4 * (size_t)bt.B * bt.Hkv;  // gmax, counters, group_done (prep_kernel)
   o = align_up(o + L.zero_bytes);
   L.cnt = o; o = align_up(o + 4 * C * G * 4);
   L.selcnt = o; o = align_up(o + 4 * C * G);
@@ -191,7 +190,6 @@ Ws carve(const Layout& L, void* base) {
   w.ovl_ret = reinterpret_cast<int*>(c + L.ovl_ret);
   w.heavy = reinterpret_cast<int*>(c + L.heavy);
   w.ovlist = reinterpret_cast<int*>(c + L.ovlist);
-  w.lbu = reinterpret_cast<uint32_t*>(c + L.lbu);
   return w;
 }
 

@@ -78,7 +78,6 @@ struct Ws {
   float* partbuf;   // [B*Hq*(D+2)]
   float* smaxbuf;   // [B*Hq]
   unsigned long long* keep;  // [chunks] block-filter masks: bit t = 128-key tile t of the chunk kept
-  uint32_t* lbu;    // [B*Hq] encoded lower bound of the DIPR max (block filter); zeroed with gmax
 };
 
 // Programmatic dependent launch: a kernel launched with the PDL attribute may

@@ -81,11 +81,8 @@ struct Stages {
   }
   static int filter(const Batch& bt, const float* q, const Ws& ws, cudaStream_t st) {
     if (bt.total_chunks == 0) return ALAYA_OK;
-    const int rows = bt.B * bt.Hq;
-    window_lb_kernel<T, D, G><<<(rows + kWarps - 1) / kWarps, kThreads, 0, st>>>(bt, q, ws);
-    block_filter_kernel<T, D, G><<<bt.total_chunks, kThreads, 0, st>>>(bt, q, ws, 0);  // LB
-    block_filter_kernel<T, D, G><<<bt.total_chunks, kThreads, 0, st>>>(bt, q, ws, 1);  // masks
-    return cuda_check("block filter");
+    return launch_pdl("block_filter_kernel", block_filter_kernel<T, D, G>, bt.total_chunks, kThreads, 0, st,
+                      bt, q, ws);
   }
   static int combine(const Batch& bt, const float* smax, const Ws& ws, float* out,
                      float* part_out, float* smax_out, cudaStream_t st) {

@@ -693,55 +693,6 @@ __device__ __forceinline__ float to_f(T x) {
   if constexpr (std::is_same_v<T, float>) return x; else return __bfloat162float(x);
 }
 
-template <typename T, int D, int G>
-__global__ void __launch_bounds__(kThreads) window_lb_kernel(const __grid_constant__ Batch bt,
-                                                             const float* __restrict__ q, Ws ws) {
-  constexpr int DL = (D + 31) / 32;
-  const int lane = threadIdx.x & 31;
-  const int row = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  if (row >= bt.B * bt.Hq) return;
-  const int b = row / bt.Hq, qh = row - b * bt.Hq, h = qh / G;
-  const KSeq& s = bt.s[b];
-  const int64_t P = s.P, off = s.off;
-  int64_t a0 = 0, a1, b0, b1;
-  if (P <= (int64_t)bt.wi + bt.wl) { a1 = P; b0 = 0; b1 = 0; }
-  else { a1 = bt.wi; b0 = P - bt.wl; b1 = P; }
-  a0 = max(a0, off) - off; a1 = min(a1, off + s.n) - off; if (a1 < a0) a1 = a0;
-  b0 = max(b0, off) - off; b1 = min(b1, off + s.n) - off; if (b1 < b0) b1 = b0;
-  const int na = (int)(a1 - a0), R = na + (int)(b1 - b0);
-  float qr[DL];
-#pragma unroll
-  for (int k = 0; k < DL; ++k) qr[k] = lane + 32 * k < D ? q[(size_t)row * D + lane + 32 * k] : 0.f;
-  const T* kb = reinterpret_cast<const T*>(s.k) + (size_t)h * s.hs;
-  float lb = -INFINITY;
-  constexpr int RU = 8;  // rows in flight
-  for (int r0 = 0; r0 < R; r0 += RU) {
-    float x[RU][DL];
-#pragma unroll
-    for (int u = 0; u < RU; ++u) {
-      const int r = r0 + u;
-      const T* kr = kb + (size_t)(r < na ? a0 + r : b0 + r - na) * D;
-#pragma unroll
-      for (int k = 0; k < DL; ++k) {
-        const int e = lane + 32 * k;
-        x[u][k] = (r < R && e < D) ? to_f(kr[e]) : 0.f;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < RU; ++u) {
-      float a = 0.f, mag = 0.f;
-#pragma unroll
-      for (int k = 0; k < DL; ++k) {
-        a = fmaf(qr[k], x[u][k], a);
-        mag = fmaf(fabsf(qr[k]), fabsf(x[u][k]), mag);
-      }
-      a = warp_sum(a);
-      mag = warp_sum(mag);
-      if (r0 + u < R) lb = fmaxf(lb, a - 1e-3f * (mag + 1.f));  // margin covers score rounding
-    }
-  }
-  if (lane == 0 && lb > -INFINITY) atomicMax(&ws.lbu[row], enc_max(lb));
-}
 
 // Per-call preparation (replaces a memset of the workspace header): zero the
 // tickets, group counters, block-filter bounds and status word, and SEED the
@@ -769,7 +720,6 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
     if (threadIdx.x == 0) *ws.status = 0;
   }
   if (threadIdx.x == 0) ws.group_done[blockIdx.x] = 0;
-  if (threadIdx.x < G) ws.lbu[b * bt.Hq + h * G + threadIdx.x] = 0u;
   float qr[G][DL];
 #pragma unroll
   for (int j = 0; j < G; ++j)
@@ -783,17 +733,33 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
   for (int j = 0; j < G; ++j) best[j] = -INFINITY;
   const int S = min(s.n, kPrepSamples);
   const T* kb = reinterpret_cast<const T*>(s.k) + (size_t)h * s.hs;
-  constexpr int RU = kPrepSamples / kWarps;  // one round of loads per warp
-  for (int i0 = warp * RU; i0 < S; i0 += kWarps * RU) {
+  // + the base window ids this shard holds (core.py:159-165): real base tokens, and
+  // the recent ones are often in the query's cluster
+  const int64_t P = s.P, off = s.off;
+  int64_t a0 = 0, a1, b0, b1;
+  if (P <= (int64_t)bt.wi + bt.wl) { a1 = P; b0 = 0; b1 = 0; }
+  else { a1 = bt.wi; b0 = P - bt.wl; b1 = P; }
+  a0 = max(a0, off) - off; a1 = min(a1, off + s.n) - off; if (a1 < a0) a1 = a0;
+  b0 = max(b0, off) - off; b1 = min(b1, off + s.n) - off; if (b1 < b0) b1 = b0;
+  const int na = (int)(a1 - a0), nbw = (int)(b1 - b0);
+  // window rows join the sample only when the block filter consumes the seed (they
+  // tighten its LB; otherwise the extra load rounds cost more than they save)
+  const int R = S + (bt.block_filter ? min(na + nbw, 2 * kPrepSamples) : 0);
+  constexpr int RU = kPrepSamples / kWarps;  // rows in flight per warp
+  for (int i0 = warp * RU; i0 < R; i0 += kWarps * RU) {
     float x[RU][DL];
 #pragma unroll
     for (int u = 0; u < RU; ++u) {
       const int i = i0 + u;
-      const T* kr = kb + (size_t)((int64_t)i * s.n / S) * D;
+      int64_t row = 0;
+      if (i < S) row = (int64_t)i * s.n / S;
+      else if (i - S < na) row = a0 + (i - S);
+      else row = b0 + (i - S - na);
+      const T* kr = kb + (size_t)row * D;
 #pragma unroll
       for (int k = 0; k < DL; ++k) {
         const int e = lane + 32 * k;
-        x[u][k] = (i < S && e < D) ? to_f(kr[e]) : 0.f;
+        x[u][k] = (i < R && e < D) ? to_f(kr[e]) : 0.f;
       }
     }
 #pragma unroll
@@ -808,7 +774,7 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
         }
         a = warp_sum(a);
         mag = warp_sum(mag);
-        if (i0 + u < S) best[j] = fmaxf(best[j], a - 1e-3f * (mag + 1.f));
+        if (i0 + u < R) best[j] = fmaxf(best[j], a - 1e-3f * (mag + 1.f));
       }
     }
   }
@@ -825,14 +791,21 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
   }
 }
 
-// Per chunk: representative-key lower bound (pass 0) or keep mask (pass 1).
+// Per chunk: keep mask of its 128-key tiles. A tile is read by the scan only if
+// some head of the group has min(box, ball) upper bound + rounding margin >=
+// LB - beta, LB = the prep seed (max score of sampled base keys and the base
+// window keys, minus a margin -- real scores, hence a lower bound of the DIPR
+// max). Exact by construction. One pass; each warp issues the bound rows of all
+// its tiles before reducing.
 template <typename T, int D, int G>
 __global__ void __launch_bounds__(kThreads) block_filter_kernel(const __grid_constant__ Batch bt,
-                                                                const float* __restrict__ q, Ws ws,
-                                                                int pass) {
+                                                                const float* __restrict__ q, Ws ws) {
   constexpr int DL = (D + 31) / 32;
+  constexpr int TPW = 2;  // tiles per warp per round (a 2048-key chunk is 16 tiles)
   __shared__ unsigned long long s_mask;
   __shared__ int s_kept;
+  pdl_trigger();
+  pdl_wait();  // the seeds come from prep_kernel
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x;
   int b, h, ci;
@@ -853,46 +826,38 @@ __global__ void __launch_bounds__(kThreads) block_filter_kernel(const __grid_con
       n2 = fmaf(qr[j][k], qr[j][k], n2);
     }
     qn[j] = sqrtf(warp_sum(n2)) * (1.f + 1e-6f);
-    thr[j] = pass ? dec_max(ws.lbu[row]) - bt.beta : 0.f;
+    thr[j] = dec_max(__ldcg(&ws.gmax[row])) - bt.beta;  // no seed: -inf keeps every tile
   }
   __syncthreads();
   const T* bb = reinterpret_cast<const T*>(s.bnd) + (size_t)h * s.bhs;
-  float lbj[G];
+  for (int t0 = warp * TPW; t0 < ntiles; t0 += kWarps * TPW) {
+    float lo[TPW][DL], hi[TPW][DL], mu[TPW][DL], rad[TPW];
 #pragma unroll
-  for (int j = 0; j < G; ++j) lbj[j] = -INFINITY;
-  for (int t = warp; t < ntiles; t += kWarps) {
-    const int blk = (ci * chunk) / 128 + t;
-    const T* lo = bb + (size_t)blk * kBndRows * D;
-    const T* hi = lo + D;
-    const T* mu = lo + 2 * D;
-    const T* rep = lo + 3 * D;
-    const float rad = to_f(lo[4 * D]);
-    bool keep = false;
+    for (int u = 0; u < TPW; ++u) {
+      const int t = min(t0 + u, ntiles - 1);
+      const T* base = bb + ((size_t)(ci * chunk) / 128 + t) * kBndRows * D;
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      if (pass == 0) {  // representative score: a real key's score
-        float a = 0.f, mag = 0.f;
+      for (int k = 0; k < DL; ++k) {
+        const int e = min(lane + 32 * k, D - 1);
+        lo[u][k] = to_f(base[e]);
+        hi[u][k] = to_f(base[D + e]);
+        mu[u][k] = to_f(base[2 * D + e]);
+      }
+      rad[u] = to_f(base[4 * D]);
+    }
 #pragma unroll
-        for (int k = 0; k < DL; ++k) {
-          const int e = lane + 32 * k;
-          if (e < D) {
-            const float x = to_f(rep[e]);
-            a = fmaf(qr[j][k], x, a);
-            mag = fmaf(fabsf(qr[j][k]), fabsf(x), mag);
-          }
-        }
-        a = warp_sum(a);
-        mag = warp_sum(mag);
-        lbj[j] = fmaxf(lbj[j], a - 1e-3f * (mag + 1.f));
-      } else {
+    for (int u = 0; u < TPW; ++u) {
+      const int t = t0 + u;
+      bool keep = false;
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
         float ubox = 0.f, qm = 0.f, mag = 0.f;
 #pragma unroll
         for (int k = 0; k < DL; ++k) {
-          const int e = lane + 32 * k;
-          if (e < D) {
-            const float m = fmaxf(qr[j][k] * to_f(lo[e]), qr[j][k] * to_f(hi[e]));
+          if (lane + 32 * k < D) {
+            const float m = fmaxf(qr[j][k] * lo[u][k], qr[j][k] * hi[u][k]);
             ubox += m;
-            const float pm = qr[j][k] * to_f(mu[e]);
+            const float pm = qr[j][k] * mu[u][k];
             qm += pm;
             mag += fabsf(m) + fabsf(pm);
           }
@@ -900,22 +865,14 @@ __global__ void __launch_bounds__(kThreads) block_filter_kernel(const __grid_con
         ubox = warp_sum(ubox);
         qm = warp_sum(qm);
         mag = warp_sum(mag);
-        const float ub = fminf(ubox, qm + qn[j] * rad);
-        keep |= ub + 1e-3f * (mag + qn[j] * rad + 1.f) >= thr[j];  // thr = -inf keeps all
+        const float ub = fminf(ubox, qm + qn[j] * rad[u]);
+        keep |= ub + 1e-3f * (mag + qn[j] * rad[u] + 1.f) >= thr[j];
+      }
+      if (t < ntiles && lane == 0 && keep) {
+        atomicOr(&s_mask, 1ull << t);
+        atomicAdd(&s_kept, 1);
       }
     }
-    if (pass == 1 && lane == 0 && keep) {
-      atomicOr(&s_mask, 1ull << t);
-      atomicAdd(&s_kept, 1);
-    }
-  }
-  if (pass == 0) {
-    if (lane < G) {
-#pragma unroll
-      for (int j = 0; j < G; ++j)
-        if (j == lane && lbj[j] > -INFINITY) atomicMax(&ws.lbu[(size_t)b * bt.Hq + h * G + j], enc_max(lbj[j]));
-    }
-    return;
   }
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -31,6 +31,7 @@ ap.add_argument("--beta", type=float, default=110.0)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--locality", action="store_true")
 ap.add_argument("--fp32", action="store_true", help="fp32 K/V (CUDA-core scan)")
+ap.add_argument("--block-filter", action="store_true", help="coarse block filter before the scan")
 ap.add_argument("--out", default=None)
 a = ap.parse_args()
 dev = torch.device("cuda")
@@ -69,9 +70,11 @@ lines = []
 for B in [int(x) for x in a.batches.split(",")]:
     hkv, d = 8, 128
     K, V, centers, g = make(B, hkv, a.ctx, d, seed=B)
-    params = engine.make_params(a.hq, hkv, d, K.dtype, a.beta, 16, 64, a.chunk, 0, 0)
-    call = engine.Call([engine.SeqView(k=K[b], v=V[b], n=a.ctx) for b in range(B)], params,
-                       K.dtype, dev)
+    params = engine.make_params(a.hq, hkv, d, K.dtype, a.beta, 16, 64, a.chunk, 0,
+                                int(a.block_filter))
+    bnd = [engine.block_bounds(K[b]) if a.block_filter else None for b in range(B)]
+    call = engine.Call([engine.SeqView(k=K[b], v=V[b], n=a.ctx, bounds=bnd[b]) for b in range(B)],
+                       params, K.dtype, dev)
     pick = torch.randint(0, 16, (B, a.hq), generator=g, device=dev)
     q = (centers[pick] + 0.25 * torch.randn(B, a.hq, d, generator=g, device=dev)).float()
     out = torch.empty_like(q)
@@ -79,7 +82,7 @@ for B in [int(x) for x in a.batches.split(",")]:
     t_scan = timed(lambda: call.scan_only(q), a.reps)
     kbytes = B * hkv * a.ctx * d * K.element_size()
     d_ = {"label": a.label, "B": B, "hq": a.hq, "ctx": a.ctx, "chunk": a.chunk,
-          "locality": a.locality, "dtype": str(K.dtype), "us_call": round(t_full, 1), "us_scan": round(t_scan, 1),
+          "locality": a.locality, "dtype": str(K.dtype), "block_filter": a.block_filter, "us_call": round(t_full, 1), "us_scan": round(t_scan, 1),
           "scan_GBps": round(kbytes / t_scan / 1e3, 1),
           "qh_per_s": round(B * a.hq / t_full * 1e6),
           "env": {k: v for k, v in os.environ.items() if k.startswith("ALAYA_")}}
