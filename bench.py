@@ -504,6 +504,9 @@ def main():
                 "gen_seconds": round(t_gen, 2)}
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()
+        if exch is not None:
+            exch.close()
         dist.destroy_process_group()
 
 

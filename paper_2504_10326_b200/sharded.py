@@ -164,6 +164,19 @@ class PeerExchange:
         if int(self.err.item()):
             raise RuntimeError("peer exchange timed out: a rank never arrived")
 
+    def close(self) -> None:
+        """Unmap the peers' buffers and free this rank's (after a barrier, so no
+        peer still writes into it)."""
+        from . import _lib
+        lib = _lib.load()
+        torch.cuda.synchronize(self.device)
+        for p in self._opened:
+            lib.alaya_exch_close(ctypes.c_void_p(p))
+        self._opened = []
+        if self.own:
+            lib.alaya_exch_free(ctypes.c_void_p(self.own))
+            self.own = 0
+
 
 def _tensor_at(ptr: int, numel: int, device: torch.device) -> torch.Tensor:
     """A float32 tensor over existing device memory (no copy, not owned)."""
