@@ -135,6 +135,7 @@ size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t zero_bytes;
+  size_t cscore_end;
   size_t status, gmax, counters, cnt, selcnt, retcnt, part_l, part_acc, cidx, cscore, partbuf, smaxbuf,
       keep, ovl_l, ovl_acc, ovl_sel, ovl_ret, heavy, ovlist, total;
 };
@@ -160,6 +161,7 @@ Layout layout_for(const Batch& bt) {
   L.ovlist = o; o = align_up(o + 4 * C * G * 3);
   L.cidx = o; o = align_up(o + 4 * C * G * bt.chunk);
   L.cscore = o; o = align_up(o + 4 * C * G * bt.chunk);
+  L.cscore_end = o;
   L.partbuf = o; o = align_up(o + 4 * rows * (D + 2));
   L.smaxbuf = o; o = align_up(o + 4 * rows);
   L.keep = o; o = align_up(o + 8 * C);
@@ -411,7 +413,15 @@ int alaya_topk(const alaya_params* p, const alaya_seq* seqs, int batch, const fl
   for (int b = 0; b < batch; ++b)
     if (seqs[b].token_offset != 0 || seqs[b].prefix_len != seqs[b].n)
       return fail(ALAYA_ERR_UNSUPPORTED, "top-k runs on unsharded sequences");
-  if ((rc = run_scan(c, d_q))) return rc;
+  // prep; the per-row candidate bound from sampled keys (scratch: the candidate
+  // score buffer, consumed before the scan writes it); the scan keeps s >= bound
+  if ((rc = c.st.prep(c.bt, d_q, c.ws, c.stream))) return rc;
+  const size_t scratch = (size_t)(c.L.cscore_end - c.L.cscore) / 4;
+  if ((rc = launch_topk_bound(c.bt, p->dtype, d_q, c.ws.cscore, scratch, k, c.ws.smaxbuf, c.stream))) return rc;
+  c.bt.topk_thr = c.ws.smaxbuf;
+  if (c.use_tc) rc = launch_tc_scan(c.bt, c.seqs, d_q, c.ws, c.stream);
+  else rc = c.st.scan(c.bt, d_q, c.ws, c.stream);
+  if (rc) return rc;
   return launch_topk_select(c.bt, c.ws, k, d_ids, d_scores, cap, d_count, c.stream);
 }
 

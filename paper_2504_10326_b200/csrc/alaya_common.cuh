@@ -47,6 +47,8 @@ struct Batch {
   int32_t split;  // attend task split threshold (candidates per (chunk, head) pair)
   int32_t seed;   // prep_kernel seeds the running max from sampled keys
   int32_t overlap;  // scan publishes per-group completion; attend runs beside it (PDL)
+  const float* topk_thr;  // TOP_K: per-row candidate threshold (a lower bound of the k-th
+                          // score) replacing max - beta in the scan; null for DIPR
 };
 
 // Coarse block indexes of a batch (kernel-parameter space).

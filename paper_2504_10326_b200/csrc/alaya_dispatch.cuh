@@ -141,6 +141,8 @@ int launch_diprs(const Batch& bt, int dtype, const alaya_graph* graphs, const fl
                  const float* floors, int cap, int64_t* ids, int64_t out_cap, int32_t* count, int32_t* explored,
                  void* ws, size_t ws_bytes, cudaStream_t st);
 constexpr int kDiprsCap = 32768;  // offered ids per sub-batch (per row scratch)
+int launch_topk_bound(const Batch& bt, int dtype, const float* q, float* scratch, size_t scratch_floats, int k,
+                      float* thr, cudaStream_t st);
 int launch_topk_select(const Batch& bt, const Ws& ws, int k, int64_t* ids, float* scores, int64_t cap,
                        int32_t* count, cudaStream_t st);
 int launch_sparse_attention(const Batch& bt, int dtype, const float* q, const int64_t* ids, int64_t cap,

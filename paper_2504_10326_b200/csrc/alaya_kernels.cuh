@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
     for (int w = 0; w < kWarps; ++w) cm = fmaxf(cm, red[w * G + tid]);
     uint32_t old = atomicMax(&ws.gmax[b * bt.Hq + h * G + tid], enc_max(cm));
     // any bound <= the true global max gives a superset of the exact set
-    thr[tid] = fmaxf(cm, dec_max(old)) - bt.beta;
+    thr[tid] = bt.topk_thr ? bt.topk_thr[b * bt.Hq + h * G + tid] : fmaxf(cm, dec_max(old)) - bt.beta;
   }
   __syncthreads();
 

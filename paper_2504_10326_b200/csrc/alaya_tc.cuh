@@ -183,11 +183,12 @@ __device__ __forceinline__ void epilogue_chunk(const Batch& bt, const Ws& ws, in
   const int chunk = bt.chunk;
   const int valid = min(chunk, bt.s[b].n - ci * chunk);
   const int ntiles = (valid + kTileKeys - 1) / kTileKeys;
-  float run[G], run0[G];
+  float run[G], run0[G], tk[G];
   int cnt[G];
 #pragma unroll
   for (int j = 0; j < G; ++j) {
     run[j] = run0[j] = dec_max(pre ? pre[j] : __ldcg(&ws.gmax[b * bt.Hq + h * G + j]));
+    tk[j] = bt.topk_thr ? __ldcg(bt.topk_thr + b * bt.Hq + h * G + j) : 0.f;
     cnt[j] = 0;
   }
   const size_t cbase = (size_t)c * G;
@@ -221,7 +222,7 @@ __device__ __forceinline__ void epilogue_chunk(const Batch& bt, const Ws& ws, in
     for (int j = 0; j < G; ++j) {
 #pragma unroll
       for (int qq = 0; qq < 4; ++qq) run[j] = fmaxf(run[j], tmax[(tb * 4 + qq) * G + j]);
-      const bool pass = ok && sc[j] >= run[j] - bt.beta;
+      const bool pass = ok && sc[j] >= (bt.topk_thr ? tk[j] : run[j] - bt.beta);
       const unsigned bal = __ballot_sync(kFull, pass);
       if (pass) {
         const int o = qoff + cnt[j] + __popc(bal & lanemask_lt());

@@ -25,6 +25,15 @@ namespace {
 
 constexpr int kSelThreads = 512;
 
+// Histogram increment aggregated over the warp's active lanes that hit the same
+// bin: radix digits of nearby scores collide heavily, and per-lane shared atomics
+// on one bin serialise.
+__device__ __forceinline__ void hist_add(unsigned* hist, unsigned bin) {
+  const unsigned act = __activemask();
+  const unsigned same = __match_any_sync(act, bin);
+  if ((threadIdx.x & 31) == (unsigned)(__ffs(same) - 1)) atomicAdd(&hist[bin], (unsigned)__popc(same));
+}
+
 // One MSB radix-select digit: among elements with (key & mask) == prefix,
 // pick the bin holding the kk-th element (descending keys if desc, else
 // ascending). Returns the bin's population; updates prefix/mask/kk.
@@ -96,7 +105,7 @@ __global__ void __launch_bounds__(kCkThreads)
     const uint32_t pre = (uint32_t)s_prefix, msk = (uint32_t)s_mask;
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
       const uint32_t u = s_key[i];
-      if ((u & msk) == pre) atomicAdd(&hist[(u >> shift) & 255], 1u);
+      if ((u & msk) == pre) hist_add(hist, (u >> shift) & 255);
     }
     pick_bin(hist, shift, true, s_prefix, s_mask, s_kk, s_found, &s_pop);
   }
@@ -112,7 +121,7 @@ __global__ void __launch_bounds__(kCkThreads)
       const uint32_t pre = (uint32_t)s_prefix, msk = (uint32_t)s_mask;
       for (int i = threadIdx.x; i < m; i += blockDim.x)
         if (s_key[i] == T && ((uint32_t)s_id[i] & msk) == pre)
-          atomicAdd(&hist[((uint32_t)s_id[i] >> shift) & 255], 1u);
+          hist_add(hist, ((uint32_t)s_id[i] >> shift) & 255);
       pick_bin(hist, shift, false, s_prefix, s_mask, s_kk, s_found, &s_pop);
     }
   }
@@ -133,6 +142,103 @@ __global__ void __launch_bounds__(kCkThreads)
     const int q = threadIdx.x;
     ws.cnt[cj * 4 + q] = max(0, min(qcap, s_n - q * qcap));
   }
+}
+
+// ---------------------------------------------------------------------------
+// TOP_K candidate bound: the k-th largest score among S evenly spaced base keys
+// of a row is <= the row's k-th largest score (a k-subset argument), so the scan
+// only needs to keep s >= that bound (minus a rounding margin) instead of every
+// token. Samples: grid (B*Hkv, ceil(S/256)), a warp per key, all G heads.
+constexpr int kMaxG = 8;
+
+template <typename T, int D>
+__global__ void __launch_bounds__(256)
+    topk_sample_kernel(const __grid_constant__ Batch bt, const float* __restrict__ q,
+                       float* __restrict__ samp, int S_max) {
+  constexpr int DL = (D + 31) / 32;
+  constexpr int RU = 8;
+  pdl_trigger();
+  pdl_wait();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b = blockIdx.x / bt.Hkv, h = blockIdx.x - b * bt.Hkv;
+  const KSeq& s = bt.s[b];
+  const int G = bt.G;
+  const int S = min(s.n, S_max);
+  float qr[kMaxG][DL];
+#pragma unroll
+  for (int j = 0; j < kMaxG; ++j)
+#pragma unroll
+    for (int k = 0; k < DL; ++k) {
+      const int e = lane + 32 * k;
+      qr[j][k] = (j < G && e < D) ? __ldg(q + ((size_t)b * bt.Hq + h * G + j) * D + e) : 0.f;
+    }
+  const T* kb = reinterpret_cast<const T*>(s.k) + (size_t)h * s.hs;
+  const int i_base = blockIdx.y * 256 + warp * 32;
+  for (int i0 = i_base; i0 < min(i_base + 32, S); i0 += RU) {
+    float x[RU][DL];
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      const int i = i0 + u;
+      const T* kr = kb + (size_t)((int64_t)min(i, S - 1) * s.n / S) * D;
+#pragma unroll
+      for (int k = 0; k < DL; ++k) {
+        const int e = lane + 32 * k;
+        x[u][k] = e < D ? to_f(kr[e]) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      const int i = i0 + u;
+#pragma unroll
+      for (int j = 0; j < kMaxG; ++j) {
+        if (j >= G) break;
+        float a = 0.f, mag = 0.f;
+#pragma unroll
+        for (int k = 0; k < DL; ++k) {
+          a = fmaf(qr[j][k], x[u][k], a);
+          mag = fmaf(fabsf(qr[j][k]), fabsf(x[u][k]), mag);
+        }
+        a = warp_sum(a);
+        mag = warp_sum(mag);
+        if (lane == 0 && i < S && i < i_base + 32)
+          samp[((size_t)b * bt.Hq + h * G + j) * S_max + i] = a - 1e-3f * (mag + 1.f);
+      }
+    }
+  }
+}
+
+// Per row: the k-th largest of its S samples -> thr[row] (-inf when S < k).
+__global__ void __launch_bounds__(256)
+    topk_thr_kernel(const __grid_constant__ Batch bt, const float* __restrict__ samp, int S_max, int k,
+                    float* __restrict__ thr) {
+  extern __shared__ uint32_t s_u[];  // [S_max]
+  __shared__ unsigned hist[256];
+  __shared__ uint64_t s_prefix, s_mask;
+  __shared__ long long s_kk;
+  __shared__ bool s_found;
+  __shared__ unsigned s_pop;
+  pdl_trigger();
+  pdl_wait();
+  const int row = blockIdx.x;
+  const int b = row / bt.Hq;
+  const int S = min(bt.s[b].n, S_max);
+  if (S < k) {
+    if (threadIdx.x == 0) thr[row] = -INFINITY;
+    return;
+  }
+  for (int i = threadIdx.x; i < S; i += blockDim.x) s_u[i] = enc_max(samp[(size_t)row * S_max + i]);
+  if (threadIdx.x == 0) { s_prefix = 0; s_mask = 0; s_kk = k; s_found = true; }
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const uint32_t pre = (uint32_t)s_prefix, msk = (uint32_t)s_mask;
+    for (int i = threadIdx.x; i < S; i += blockDim.x) {
+      const uint32_t u = s_u[i];
+      if ((u & msk) == pre) hist_add(hist, (u >> shift) & 255);
+    }
+    pick_bin(hist, shift, true, s_prefix, s_mask, s_kk, s_found, &s_pop);
+  }
+  if (threadIdx.x == 0) thr[row] = dec_max((uint32_t)s_prefix);
 }
 
 // Exact top-k of each row over the scan candidate lists (the scan ran with
@@ -211,7 +317,7 @@ __global__ void __launch_bounds__(kSelThreads)
       uint32_t u;
       int lid;
       elem(e, u, lid);
-      if ((u & msk) == pre) atomicAdd(&hist[(u >> shift) & 255], 1u);
+      if ((u & msk) == pre) hist_add(hist, (u >> shift) & 255);
     }
     pick_bin(hist, shift, true, s_prefix, s_mask, s_kk, s_found, &s_pop);
     if (!s_found) break;  // fewer than k candidates: take them all
@@ -233,7 +339,7 @@ __global__ void __launch_bounds__(kSelThreads)
         uint32_t u;
         int lid;
         elem(e, u, lid);
-        if (u == T && ((uint32_t)lid & msk) == pre) atomicAdd(&hist[((uint32_t)lid >> shift) & 255], 1u);
+        if (u == T && ((uint32_t)lid & msk) == pre) hist_add(hist, ((uint32_t)lid >> shift) & 255);
       }
       pick_bin(hist, shift, false, s_idprefix, s_idmask, s_kk, s_found, &s_pop);
     }
@@ -364,7 +470,7 @@ __global__ void __launch_bounds__(kSelThreads)
     const uint32_t pre = (uint32_t)s_prefix, msk = (uint32_t)s_mask;
     for (int i = threadIdx.x; i < nb; i += blockDim.x) {
       const uint32_t u = s_score[i];
-      if ((u & msk) == pre) atomicAdd(&hist[(u >> shift) & 255], 1u);
+      if ((u & msk) == pre) hist_add(hist, (u >> shift) & 255);
     }
     pick_bin(hist, shift, true, s_prefix, s_mask, s_kk, s_found, &s_pop);
     if (!s_found) break;
@@ -382,7 +488,7 @@ __global__ void __launch_bounds__(kSelThreads)
       const uint32_t pre = (uint32_t)s_idprefix, msk = (uint32_t)s_idmask;
       for (int i = threadIdx.x; i < nb; i += blockDim.x)
         if (s_score[i] == Tk && ((uint32_t)i & msk) == pre)
-          atomicAdd(&hist[((uint32_t)i >> shift) & 255], 1u);
+          hist_add(hist, ((uint32_t)i >> shift) & 255);
       pick_bin(hist, shift, false, s_idprefix, s_idmask, s_kk, s_found, &s_pop);
     }
   }
@@ -608,6 +714,37 @@ int block_topk_d(const Batch& bt, const float* q, const BixSet& bix, int max_nb,
 }
 
 }  // namespace
+
+int launch_topk_bound(const Batch& bt, int dtype, const float* q, float* scratch, size_t scratch_floats, int k,
+                      float* thr, cudaStream_t st) {
+  int max_n = 0;
+  for (int b = 0; b < bt.B; ++b) max_n = std::max(max_n, bt.s[b].n);
+  // 16 samples per wanted token, 4096..8192 per row, within the scratch (fewer samples
+  // loosen the bound: 1024 measured slower overall at k=100)
+  int S_max = std::min(std::max(16 * k, 4096), 8192);
+  S_max = std::min<int64_t>(S_max, std::max(max_n, 1));
+  S_max = (int)std::min<size_t>((size_t)S_max, scratch_floats / (size_t)(bt.B * bt.Hq));
+  if (S_max < 1) S_max = 1;
+  const dim3 grid(bt.B * bt.Hkv, (S_max + 255) / 256);
+  int rc;
+  if (bt.G > kMaxG) return fail(ALAYA_ERR_UNSUPPORTED, "group size %d > 8", bt.G);
+#define ALAYA_SAMPLE(TT, DD) \
+  rc = launch_pdl("topk_sample_kernel", topk_sample_kernel<TT, DD>, grid, 256, 0, st, bt, q, scratch, S_max)
+  const bool bf = dtype == ALAYA_BF16;
+  switch (bt.D) {
+    case 16: if (bf) ALAYA_SAMPLE(__nv_bfloat16, 16); else ALAYA_SAMPLE(float, 16); break;
+    case 32: if (bf) ALAYA_SAMPLE(__nv_bfloat16, 32); else ALAYA_SAMPLE(float, 32); break;
+    case 64: if (bf) ALAYA_SAMPLE(__nv_bfloat16, 64); else ALAYA_SAMPLE(float, 64); break;
+    case 128: if (bf) ALAYA_SAMPLE(__nv_bfloat16, 128); else ALAYA_SAMPLE(float, 128); break;
+    default: if (bf) ALAYA_SAMPLE(__nv_bfloat16, 256); else ALAYA_SAMPLE(float, 256); break;
+  }
+#undef ALAYA_SAMPLE
+  if (rc) return rc;
+  const size_t smem = (size_t)S_max * 4;
+  cudaFuncSetAttribute(topk_thr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return launch_pdl("topk_thr_kernel", topk_thr_kernel, (unsigned)(bt.B * bt.Hq), 256, smem, st, bt, scratch,
+                    S_max, k, thr);
+}
 
 int launch_topk_select(const Batch& bt, const Ws& ws, int k, int64_t* ids, float* scores, int64_t cap,
                        int32_t* count, cudaStream_t st) {
