@@ -1,0 +1,33 @@
+"""The multi-rank bench path in real processes (2 ranks sharing one GPU, gloo
+for the host collectives): the peer-memory exchange's CUDA IPC mapping and its
+cross-process flag protocol, validated against NCCL-free host collectives, and
+the sharded result against the unsharded kernels (bench.py --check)."""
+
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+@pytest.mark.parametrize("p2p", ["1", "0"])
+def test_two_process_sharded_bench_check(cuda_ok, p2p):
+    env = dict(os.environ, ALAYA_BENCH_SHARE_GPU="1", ALAYA_P2P=p2p)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + int(p2p)), "bench.py",
+           "--gpus", "2", "--steps", "1", "--warmup", "3", "--layers", "2", "--ctx", "8192",
+           "--batch", "2", "--check", "--no-e2e", "--no-cpu"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
+    d = json.loads(line)
+    assert d["sharded_check"]["ok"], d["sharded_check"]
+    assert d["config"]["collectives"] == ("p2p" if p2p == "1" else "nccl")
