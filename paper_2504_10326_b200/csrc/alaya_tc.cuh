@@ -420,13 +420,15 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 4 : (kStages <= 3 
       int b, h;
       epilogue_chunk<G, NP>(bt, ws, c, quarter, lane, tmem_base, accf0, acce0, acc, aphase, b, h,
                             tmax, tcount, cur);
-      if (bt.overlap) {  // this warp's candidates, counts, heavy flags and max are
-        __threadfence();  // visible GPU-wide before its group counter moves
-        __syncwarp();
-        if (lane == 0) {
-          atomicAdd(&ws.group_done[b * bt.Hkv + h], 1);
-          atomicAdd(&ws.counters[6], 1);
-        }
+      if (bt.overlap && quarter == 0) __syncwarp();  // lanes 1..G-1 wrote heavy flags
+      if (bt.overlap && quarter == 0 && lane == 0) {
+        // the chunk is published once, by quarter 0 after the epilogue's final named
+        // barrier (every warp's candidates and counts, its own heavy flags): a
+        // release add makes them visible before the group counter moves (the
+        // barrier + single release-store pattern of CUTLASS's semaphore)
+        asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(&ws.group_done[b * bt.Hkv + h]), "r"(4)
+                     : "memory");
+        asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(&ws.counters[6]), "r"(4) : "memory");
       }
     }
   }
