@@ -331,7 +331,7 @@ def main():
         agree = torch.tensor([1 if ok else 0], device=dev if not share else "cpu")
         dist.all_reduce(agree, op=dist.ReduceOp.MIN)
         if int(agree.item()):
-            collective = "p2p"
+            collective = "p2p-fused" if getattr(stages[0], "fused_used", False) else "p2p"
         else:
             exch = None
 
@@ -496,9 +496,10 @@ def main():
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 # per layer: window append + (single GPU) prep, scan, attend, combine, or
                 # (sharded) prep, scan, combine (local max), attend, combine (partial), merge
-                # + 2 exchanges (peer path; NCCL's own kernels not counted)
+                # + 2 exchanges (peer path; NCCL's own kernels not counted), or (fused
+                # peer path) prep, scan, attend, combine, allgather, merge
                 "gpu_launches": a.steps * L * (5 if world == 1 else
-                                               (9 if collective == "p2p" else 7)),
+                                               {"p2p": 9, "p2p-fused": 7}.get(collective, 7)),
                 "clocks": sampler.summary(), "parity": parity, "stats": stats,
                 "sharded_check": sharded_check,
                 "gen_seconds": round(t_gen, 2)}

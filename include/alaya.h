@@ -141,6 +141,23 @@ int alaya_attend(const alaya_params* p, const alaya_seq* seqs, int batch, const 
                  const float* d_smax, float* d_part, int want_values, void* d_ws,
                  size_t ws_bytes, void* stream);
 
+/* Stages 1+2 fused for the sharded step (replaces scan -> allreduce(MAX) ->
+ * attend of sharded.py; reference dipr.py:64 global max over all shards):
+ * the CTA completing a (seq, kv head) group's scan stores the group's local
+ * maxima straight into every rank's exchange buffer (bufs: the n_ranks
+ * symmetric buffers of alaya_exch_alloc/open, NVLink P2P) and raises a
+ * per-group flag to `epoch`; the attend kernel, running beside the scan, waits
+ * for the n_ranks flags of each group it filters, takes the max over the
+ * ranks' slots and filters at that global max - beta. Writes d_part as
+ * alaya_attend does. Every rank calls it with the same epoch (the kind-0
+ * epoch counter of alaya_exch: slots of parity epoch&1, kind 0). A rank that
+ * never arrives sets *d_err = 1 after a bounded poll. ALAYA_ERR_UNSUPPORTED
+ * when the call is not tcgen05-eligible (use the staged path). */
+int alaya_sharded_step(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q,
+                       void* const* bufs, int n_ranks, int rank, int64_t cap_floats,
+                       unsigned long long epoch, float* d_part, int* d_err, void* d_ws,
+                       size_t ws_bytes, void* stream);
+
 /* Stage 3: merge n_parts partial sets (d_parts: [n_parts][batch*Hq][dim+2]) in
  * order and finalize to d_out [batch*Hq][dim] fp32. Non-finite output sets
  * *d_status (device int) to ALAYA_ERR_NONFINITE. */

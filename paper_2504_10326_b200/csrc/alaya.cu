@@ -341,6 +341,34 @@ int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch
   return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);
 }
 
+int alaya_sharded_step(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q,
+                       void* const* bufs, int n_ranks, int rank, int64_t cap_floats, unsigned long long epoch,
+                       float* d_part, int* d_err, void* d_ws, size_t ws_bytes, void* stream) {
+  Call c;
+  int rc = prepare(p, seqs, batch, d_ws, ws_bytes, stream, &c);
+  if (rc) return rc;
+  if (!d_q || !d_part || !bufs) return fail(ALAYA_ERR_ARG, "null q/part/bufs");
+  if (n_ranks < 1 || n_ranks > kExMaxPeers || rank < 0 || rank >= n_ranks)
+    return fail(ALAYA_ERR_ARG, "bad ranks %d/%d", rank, n_ranks);
+  if (!c.use_tc) return fail(ALAYA_ERR_UNSUPPORTED, "fused sharded step needs the tcgen05 scan");
+  if ((int64_t)c.bt.B * c.bt.Hq > cap_floats || c.bt.B * c.bt.Hkv > kExGroups)
+    return fail(ALAYA_ERR_SHAPE, "fused sharded step: %d rows / %d groups beyond the exchange buffer",
+                c.bt.B * c.bt.Hq, c.bt.B * c.bt.Hkv);
+  for (int r = 0; r < n_ranks; ++r)
+    if (!bufs[r]) return fail(ALAYA_ERR_ARG, "null peer buffer %d", r);
+  c.bt.overlap = 1;
+  c.bt.sx_on = 1;
+  for (int r = 0; r < n_ranks; ++r) c.bt.sx.peers[r] = static_cast<char*>(bufs[r]);
+  c.bt.sx.rank = rank;
+  c.bt.sx.R = n_ranks;
+  c.bt.sx.cap = cap_floats;
+  c.bt.sx.epoch = epoch;
+  c.bt.sx.err = d_err;
+  if ((rc = run_scan(c, d_q))) return rc;
+  if ((rc = c.st.attend_ovl(c.bt, d_q, c.ws, c.stream))) return rc;
+  return c.st.combine(c.bt, c.ws.smaxbuf, c.ws, nullptr, d_part, nullptr, c.stream);
+}
+
 int alaya_scan(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q,
                float* d_smax, void* d_ws, size_t ws_bytes, void* stream) {
   Call c;

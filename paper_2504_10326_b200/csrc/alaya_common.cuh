@@ -35,6 +35,37 @@ struct KSeq {
   int64_t bhs;
 };
 
+// Sequence-sharded step with the collectives fused into the kernels (peer
+// memory): the tcgen05 scan's CTA that completes a (sequence, kv head) group
+// stores the group's local maxima into every rank's exchange buffer and raises
+// the group's flag there; attend tasks start once every rank's flag for their
+// group is up (alaya_exch.cu has the buffer layout).
+constexpr int kExMaxPeers = 16;
+constexpr size_t kExFlagBytes = 512;        // kind flags + arrival counter
+constexpr int kExGroups = 4096;             // per-group flags [kExGroups][kExMaxPeers] u64
+struct ShardExch {
+  char* peers[kExMaxPeers];
+  int32_t rank, R;
+  int64_t cap;                 // floats per slot
+  unsigned long long epoch;    // this step's epoch (same on every rank)
+  int* err;                    // set to 1 when a rank never arrived (bounded poll)
+};
+__device__ __forceinline__ float* exch_slot(char* buf, int parity, int kind, int r, int R, int64_t cap) {
+  float* base = reinterpret_cast<float*>(buf + kExFlagBytes + (size_t)kExGroups * kExMaxPeers * 8);
+  return base + ((((size_t)parity * 2 + kind) * R + r) * (size_t)cap);
+}
+__device__ __forceinline__ unsigned long long* exch_gflag(char* buf, int g, int r) {
+  return reinterpret_cast<unsigned long long*>(buf + kExFlagBytes) + (size_t)g * kExMaxPeers + r;
+}
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 struct Batch {
   KSeq s[ALAYA_MAX_BATCH];
   int32_t B, Hq, Hkv, G, D, chunk;
@@ -49,6 +80,8 @@ struct Batch {
   int32_t overlap;  // scan publishes per-group completion; attend runs beside it (PDL)
   const float* topk_thr;  // TOP_K: per-row candidate threshold (a lower bound of the k-th
                           // score) replacing max - beta in the scan; null for DIPR
+  int32_t sx_on;          // fused sharded step (needs overlap): see ShardExch
+  ShardExch sx;
 };
 
 // Coarse block indexes of a batch (kernel-parameter space).

@@ -30,8 +30,10 @@ struct Peers {
 };
 
 // symmetric buffer: [2 kinds][kMaxPeers] u64 flags + an arrival counter (u64
-// slot), padded to 512 B, then slots: [parity 2][kind 2][R][cap] floats
-constexpr size_t kFlagBytes = 512;
+// slot), padded to 512 B; per-group flags [kExGroups][kMaxPeers] u64 (fused
+// sharded step); then slots: [parity 2][kind 2][R][cap] floats
+constexpr size_t kFlagBytes = kExFlagBytes;
+constexpr size_t kHeadBytes = kExFlagBytes + (size_t)kExGroups * kExMaxPeers * 8;
 
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -43,8 +45,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 }
 
 __device__ __forceinline__ float* slot(char* buf, int parity, int kind, int r, int R, int64_t cap) {
-  float* base = reinterpret_cast<float*>(buf + kFlagBytes);
-  return base + ((((size_t)parity * 2 + kind) * R + r) * (size_t)cap);
+  return exch_slot(buf, parity, kind, r, R, cap);
 }
 
 // Allgather of larger messages (e.g. 0.5 MB of partial states per rank at 32
@@ -154,7 +155,7 @@ extern "C" {
 
 size_t alaya_exch_bytes(int n_ranks, int64_t cap_floats) {
   if (n_ranks < 1 || n_ranks > kMaxPeers || cap_floats < 1) return 0;
-  return kFlagBytes + (size_t)2 * 2 * n_ranks * (size_t)cap_floats * 4;
+  return kHeadBytes + (size_t)2 * 2 * n_ranks * (size_t)cap_floats * 4;
 }
 
 int alaya_exch_alloc(size_t bytes, void** d_buf, void* ipc_handle) {
@@ -212,7 +213,7 @@ int alaya_exch(void* const* bufs, int n_ranks, int rank, int64_t cap_floats, int
 
 float* alaya_exch_slots(void* d_buf, int n_ranks, int64_t cap_floats, int kind, unsigned long long epoch) {
   if (!d_buf) return nullptr;
-  float* base = reinterpret_cast<float*>(static_cast<char*>(d_buf) + kFlagBytes);
+  float* base = reinterpret_cast<float*>(static_cast<char*>(d_buf) + kHeadBytes);
   return base + (((size_t)(epoch & 1ull) * 2 + kind) * n_ranks) * (size_t)cap_floats;
 }
 

@@ -503,6 +503,32 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
+// Fused sharded step: wait until every rank raised the flag of group (b, h) in
+// this rank's exchange buffer, then the global max of row (b, h*G + j) = max of
+// the R ranks' local maxima, into ws.smaxbuf (every warp computing it writes the
+// same value).
+__device__ __forceinline__ void sx_global_max(const Batch& bt, const Ws& ws, int b, int h, int j, int lane) {
+  const ShardExch& x = bt.sx;
+  const int g = b * bt.Hkv + h, row = b * bt.Hq + h * bt.G + j;
+  const int parity = (int)(x.epoch & 1ull);
+  float m = -INFINITY;
+  if (lane < x.R) {
+    const unsigned long long* f = exch_gflag(x.peers[x.rank], g, lane);
+    long long polls = 0;
+    while (ld_acquire_sys_u64(f) < x.epoch) {
+      if (++polls > (1ll << 26)) {  // a rank never arrived: flag the call, use what is here
+        if (x.err) atomicExch(x.err, 1);
+        break;
+      }
+      __nanosleep(128);
+    }
+    m = __ldcv(exch_slot(x.peers[x.rank], parity, 0, lane, x.R, x.cap) + row);
+  }
+  m = warp_max(m);
+  if (lane == 0) ws.smaxbuf[row] = m;
+  __syncwarp();
+}
+
 // Attend launched BESIDE the tcgen05 scan (bt.overlap): the kernel is a PDL
 // dependent of the scan and skips the grid-dependency wait; the scan only
 // triggers after its own wait, so everything before the scan is complete.
@@ -538,11 +564,15 @@ __global__ void __launch_bounds__(kOvlThreads, 4)  // <= 128 regs: one CTA fits 
       cj = task - nwin;
       int b, h, ci;
       decode_chunk(bt, (int)cj / G, b, h, ci);
-      if (lane == 0) {
-        const int* gd = ws.group_done + b * bt.Hkv + h;
-        while (ld_acquire_gpu(gd) < 4 * bt.s[b].nch) __nanosleep(256);
+      if (bt.sx_on) {
+        sx_global_max(bt, ws, b, h, (int)(cj - (cj / G) * G), lane);
+      } else {
+        if (lane == 0) {
+          const int* gd = ws.group_done + b * bt.Hkv + h;
+          while (ld_acquire_gpu(gd) < 4 * bt.s[b].nch) __nanosleep(256);
+        }
+        __syncwarp();
       }
-      __syncwarp();
       qe = __ldcg(&ws.heavy[cj]) ? 1 : 4;
     } else {
       if (novl < 0) {  // overflow items are final once every chunk has published
@@ -557,8 +587,14 @@ __global__ void __launch_bounds__(kOvlThreads, 4)  // <= 128 regs: one CTA fits 
       cj = (size_t)(item >> 2);
       qb = item & 3;
       qe = qb + 1;
+      if (bt.sx_on) {
+        int b, h, ci;
+        decode_chunk(bt, (int)cj / G, b, h, ci);
+        sx_global_max(bt, ws, b, h, (int)(cj - (cj / G) * G), lane);
+      }
     }
-    sel_task_pipe<T, D, G, true>(bt, nullptr, ws, cj, qb, qe, lane, s_t[warp], s_w[warp], true);
+    sel_task_pipe<T, D, G, true>(bt, bt.sx_on ? ws.smaxbuf : nullptr, ws, cj, qb, qe, lane, s_t[warp],
+                                 s_w[warp], true);
   }
 }
 
@@ -720,6 +756,17 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
     if (threadIdx.x == 0) *ws.status = 0;
   }
   if (threadIdx.x == 0) ws.group_done[blockIdx.x] = 0;
+  if (bt.sx_on && s.nch == 0) {  // fused sharded step: no chunk will complete this group
+    const ShardExch& x = bt.sx;
+    const int parity = (int)(x.epoch & 1ull);
+    if (threadIdx.x < G * x.R) {
+      const int j = threadIdx.x % G, r = threadIdx.x / G;
+      exch_slot(x.peers[r], parity, 0, x.rank, x.R, x.cap)[b * bt.Hq + h * G + j] = -INFINITY;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x < x.R) st_release_sys_u64(exch_gflag(x.peers[threadIdx.x], blockIdx.x, x.rank), x.epoch);
+  }
   float qr[G][DL];
 #pragma unroll
   for (int j = 0; j < G; ++j)

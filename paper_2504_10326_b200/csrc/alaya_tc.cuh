@@ -420,15 +420,39 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 4 : (kStages <= 3 
       int b, h;
       epilogue_chunk<G, NP>(bt, ws, c, quarter, lane, tmem_base, accf0, acce0, acc, aphase, b, h,
                             tmax, tcount, cur);
-      if (bt.overlap && quarter == 0) __syncwarp();  // lanes 1..G-1 wrote heavy flags
-      if (bt.overlap && quarter == 0 && lane == 0) {
+      if (bt.overlap && quarter == 0) {
+        __syncwarp();  // lanes 1..G-1 wrote heavy flags
         // the chunk is published once, by quarter 0 after the epilogue's final named
         // barrier (every warp's candidates and counts, its own heavy flags): a
         // release add makes them visible before the group counter moves (the
         // barrier + single release-store pattern of CUTLASS's semaphore)
-        asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(&ws.group_done[b * bt.Hkv + h]), "r"(4)
-                     : "memory");
-        asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(&ws.counters[6]), "r"(4) : "memory");
+        int old = 0;
+        if (lane == 0) {
+          if (bt.sx_on) {
+            asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;"
+                         : "=r"(old) : "l"(&ws.group_done[b * bt.Hkv + h]), "r"(4) : "memory");
+          } else {
+            asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(&ws.group_done[b * bt.Hkv + h]),
+                         "r"(4) : "memory");
+          }
+          asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(&ws.counters[6]), "r"(4) : "memory");
+        }
+        if (bt.sx_on) {
+          old = __shfl_sync(kFull, old, 0);
+          if (old + 4 == 4 * bt.s[b].nch) {  // this chunk completed the group: its maxima are
+            const ShardExch& x = bt.sx;    // final -> every rank's slot, then the group flag
+            const int parity = (int)(x.epoch & 1ull);
+            const int g = b * bt.Hkv + h;
+            for (int i = lane; i < G * x.R; i += 32) {
+              const int j = i % G, r = i / G;
+              const float m = dec_max(__ldcg(&ws.gmax[b * bt.Hq + h * G + j]));
+              exch_slot(x.peers[r], parity, 0, x.rank, x.R, x.cap)[b * bt.Hq + h * G + j] = m;
+            }
+            __threadfence_system();
+            __syncwarp();
+            if (lane < x.R) st_release_sys_u64(exch_gflag(x.peers[lane], g, x.rank), x.epoch);
+          }
+        }
       }
     }
   }

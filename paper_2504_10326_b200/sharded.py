@@ -25,6 +25,7 @@ CPU (gloo) tests can drive it with a host double; the product path passes
 from __future__ import annotations
 
 import ctypes
+import os
 from typing import Protocol
 
 import torch
@@ -71,6 +72,20 @@ class EngineStages:
     def merge(self, parts):
         return engine.merge_partials(parts, self.dim)
 
+    def fused(self, q, exchange: "PeerExchange"):
+        """Scan -> max over peers -> attend as one launch sequence (the max
+        travels over NVLink per (seq, kv head) group as the scan completes it).
+        ``None`` when not eligible."""
+        if q.shape[0] * q.shape[1] > exchange.cap:
+            return None
+        e = exchange.epoch[0] + 1
+        part = self.call.sharded_step(q, exchange._arr, exchange.world, exchange.rank, exchange.cap,
+                                      e, exchange.err)
+        if part is not None:
+            exchange.epoch[0] = e
+        self.fused_used = part is not None
+        return part
+
 
 def _staged(t: torch.Tensor, group) -> tuple[torch.Tensor, bool]:
     """gloo cannot run these collectives on CUDA tensors: stage through host."""
@@ -93,6 +108,7 @@ class PeerExchange:
         self.device = device
         self._opened = opened
         self.epoch = [0, 0]
+        self.fused = os.environ.get("ALAYA_FUSED_SHARD", "1") != "0"  # scan+max+attend fused
         self.err = torch.zeros(1, dtype=torch.int32, device=device)
         self._arr = (ctypes.c_void_p * world)(*bufs)
 
@@ -192,8 +208,11 @@ def sharded_attention(stages: LocalStages, q: torch.Tensor, group=None,
     (identical on every rank). With ``exchange`` the two collectives run over
     peer memory (``alaya_exch``), otherwise through ``torch.distributed``."""
     if exchange is not None:
-        smax = exchange.allreduce_max(stages.scan(q))
-        part = stages.attend(q, smax).contiguous()
+        fused = getattr(stages, "fused", None) if exchange.fused else None
+        part = fused(q, exchange) if fused is not None else None
+        if part is None:
+            smax = exchange.allreduce_max(stages.scan(q))
+            part = stages.attend(q, smax).contiguous()
         parts = exchange.allgather(part)
         out = stages.merge(parts)
         return out.view(q.shape[0], q.shape[1], -1)

@@ -18,11 +18,13 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 
 
-@pytest.mark.parametrize("p2p", ["1", "0"])
-def test_two_process_sharded_bench_check(cuda_ok, p2p):
-    env = dict(os.environ, ALAYA_BENCH_SHARE_GPU="1", ALAYA_P2P=p2p)
+@pytest.mark.parametrize("p2p,fused", [("1", "1"), ("1", "0"), ("0", "0")])
+def test_two_process_sharded_bench_check(cuda_ok, p2p, fused):
+    """p2p=1 fused=1: scan -> max over peer memory -> attend fused
+    (alaya_sharded_step); fused=0: staged alaya_exch collectives; p2p=0: NCCL."""
+    env = dict(os.environ, ALAYA_BENCH_SHARE_GPU="1", ALAYA_P2P=p2p, ALAYA_FUSED_SHARD=fused)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(29600 + int(p2p)), "bench.py",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + 2 * int(p2p) + int(fused)), "bench.py",
            "--gpus", "2", "--steps", "1", "--warmup", "3", "--layers", "2", "--ctx", "8192",
            "--batch", "2", "--check", "--no-e2e", "--no-cpu"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
@@ -30,4 +32,5 @@ def test_two_process_sharded_bench_check(cuda_ok, p2p):
     line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
     d = json.loads(line)
     assert d["sharded_check"]["ok"], d["sharded_check"]
-    assert d["config"]["collectives"] == ("p2p" if p2p == "1" else "nccl")
+    want = {("1", "1"): "p2p-fused", ("1", "0"): "p2p", ("0", "0"): "nccl"}[(p2p, fused)]
+    assert d["config"]["collectives"] == want

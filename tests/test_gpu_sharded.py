@@ -179,3 +179,55 @@ def test_sharded_attention_over_peer_exchange(cuda_ok):
     from paper_2504_10326_b200 import _lib
     for b in bufs:
         _lib.load().alaya_exch_free(b)
+
+
+def test_fused_sharded_step_emulated(cuda_ok):
+    """alaya_sharded_step (scan -> per-group max over peer memory -> attend) for
+    2 ranks emulated on streams of one GPU at a size whose grids co-reside (each
+    rank's attend waits on the other's scan: the bounded poll turns a missed
+    arrival into the error flag, not a hang), vs the unsharded kernels."""
+    from paper_2504_10326_b200 import _lib, engine
+    from paper_2504_10326_b200.sharded import EngineStages, local_view
+    dev = torch.device("cuda")
+    world, B, hkv, g, d, n, w, beta = 2, 2, 2, 4, 128, 6000, 3, 5.0
+    dtype = torch.bfloat16
+    r = np.random.default_rng(9)
+    K, V, WK, WV, qs = [], [], [], [], []
+    for b in range(B):
+        _, k, v, centers, _ = O.make_context(n + 1000 * b, 1, hkv, d, seed=700 + b)
+        K.append(torch.from_numpy(O.bf16_round(k)[0]).to(dev, dtype))
+        V.append(torch.from_numpy(O.bf16_round(v)[0]).to(dev, dtype))
+        WK.append(torch.randn(hkv, w, d, device=dev).to(dtype))
+        WV.append(torch.randn(hkv, w, d, device=dev).to(dtype))
+        qs.append(centers[r.integers(0, 16, hkv * g)] + 0.25 * r.standard_normal((hkv * g, d)))
+    q = torch.tensor(np.stack(qs), dtype=torch.float32, device=dev)
+    params = engine.make_params(hkv * g, hkv, d, dtype, beta, 16, 64)
+    full = engine.Call([engine.SeqView(k=K[b], v=V[b], n=K[b].shape[1], wk=WK[b], wv=WV[b], w=w)
+                        for b in range(B)], params, dtype, dev,
+                       ws=torch.empty(1, dtype=torch.uint8, device=dev))
+    o_full = full.dipr_attention(q).clone()
+    stages = [EngineStages([local_view(K[b], V[b], world, rk, WK[b], WV[b], w) for b in range(B)],
+                           params, dtype, dev) for rk in range(world)]
+    for st in stages:
+        st.call.ws = torch.empty(st.call.ws_bytes, dtype=torch.uint8, device=dev)
+    exs, bufs = _exchange_group(world, B * hkv * g * (d + 2), dev)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    torch.cuda.synchronize()
+    for _ in range(3):
+        parts, outs = [None] * world, [None] * world
+        for rk in range(world):
+            with torch.cuda.stream(streams[rk]):
+                parts[rk] = stages[rk].fused(q, exs[rk])
+                assert parts[rk] is not None and stages[rk].fused_used
+        for rk in range(world):
+            with torch.cuda.stream(streams[rk]):
+                parts[rk] = exs[rk].allgather(parts[rk])
+        for rk in range(world):
+            with torch.cuda.stream(streams[rk]):
+                outs[rk] = stages[rk].merge(parts[rk]).view(q.shape[0], q.shape[1], -1)
+        torch.cuda.synchronize()
+        for rk in range(world):
+            exs[rk].check()
+            assert float(((outs[rk] - o_full).norm() / o_full.norm()).item()) <= 2e-6
+    for b in bufs:
+        _lib.load().alaya_exch_free(b)
