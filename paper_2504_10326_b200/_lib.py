@@ -13,6 +13,8 @@ from pathlib import Path
 
 LIB_NAME = "libalaya_b200.so"
 LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+if os.environ.get("ALAYA_LIB_VARIANT"):  # diagnostics: an in-tree build variant (tools/variants.sh)
+    LIB_PATH = Path(__file__).resolve().parent / "variants" / os.environ["ALAYA_LIB_VARIANT"] / LIB_NAME
 
 ALAYA_OK = 0
 ALAYA_ERR_ARG = 1

@@ -233,6 +233,7 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
 // selection partial is the (global) max, so chunk partials merge by plain sums.
 // ---------------------------------------------------------------------------
 constexpr int kGatherU = 16;  // V rows in flight per half-warp (one candidate batch)
+static_assert(2 * kGatherU == 32, "one 32-candidate filter batch = kGatherU rows per half-warp");
 
 constexpr int kWinU = 4;     // window rows in flight per half-warp
 
