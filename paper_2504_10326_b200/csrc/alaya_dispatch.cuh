@@ -86,8 +86,15 @@ struct Stages {
   }
   static int combine(const Batch& bt, const float* smax, const Ws& ws, float* out,
                      float* part_out, float* smax_out, cudaStream_t st) {
+    // one CTA per row; few rows -> more warps per row (chunk partials in flight)
     const int rows = bt.B * bt.Hq;
-    return launch_pdl("combine_kernel", combine_kernel<D, G>, rows, kThreads, 0, st, bt, smax, ws, out,
+    if (rows <= num_sms() / 2)
+      return launch_pdl("combine_kernel", combine_kernel<D, G, 32>, rows, 1024, 0, st, bt, smax, ws, out,
+                        part_out, smax_out);
+    if (rows <= num_sms() + num_sms() / 2)
+      return launch_pdl("combine_kernel", combine_kernel<D, G, 16>, rows, 512, 0, st, bt, smax, ws, out,
+                        part_out, smax_out);
+    return launch_pdl("combine_kernel", combine_kernel<D, G, 8>, rows, 256, 0, st, bt, smax, ws, out,
                       part_out, smax_out);
   }
 };

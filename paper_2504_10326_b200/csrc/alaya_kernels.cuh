@@ -606,16 +606,16 @@ __global__ void __launch_bounds__(kOvlThreads, 4)  // <= 128 regs: one CTA fits 
 // selected first, then window), finalized (attention.py:145-152) or exported
 // as (m, l, acc) for a cross-shard merge.
 // ---------------------------------------------------------------------------
-template <int D, int G>
-__global__ void __launch_bounds__(kThreads)
+template <int D, int G, int CW>
+__global__ void __launch_bounds__(CW * 32)
     combine_kernel(const __grid_constant__ Batch bt, const float* __restrict__ smax_ext, Ws ws,
                    float* __restrict__ out, float* __restrict__ part_out,
                    float* __restrict__ smax_out) {
   constexpr int DL = (D + 31) / 32;
   constexpr int U = 4;
-  __shared__ float red[kWarps][D];
-  __shared__ float redl[kWarps];
-  __shared__ int redn[kWarps];
+  __shared__ float red[CW][D];
+  __shared__ float redl[CW];
+  __shared__ int redn[CW];
   pdl_trigger();
   pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -629,12 +629,12 @@ __global__ void __launch_bounds__(kThreads)
   for (int k = 0; k < DL; ++k) ab[k] = 0.f;
   float lb = 0.f;
   int nsel = 0;
-  for (int c = warp; c < s.nch; c += kWarps * U) {
+  for (int c = warp; c < s.nch; c += CW * U) {
     float v[U][DL], pl[U];
     int tot[U], ps[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {  // issue every load of the batch first
-      const int cc = c + u * kWarps;
+      const int cc = c + u * CW;
       const size_t cj = (size_t)(c0 + cc) * G + j;
       tot[u] = cc < s.nch ? ws.heavy[cj] : 0;
       pl[u] = cc < s.nch ? ws.part_l[cj] : 0.f;
@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(kThreads)
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int cc = c + u * kWarps;
+      const int cc = c + u * CW;
       const size_t cj = (size_t)(c0 + cc) * G + j;
       if (cc < s.nch && tot[u]) {  // overflow sub-lists of a heavy pair
         for (int sq = 1; sq < 4; ++sq) {
@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(kThreads)
   lb = 0.f;
   nsel = 0;
 #pragma unroll
-  for (int w = 0; w < kWarps; ++w) { lb += redl[w]; nsel += redn[w]; }
+  for (int w = 0; w < CW; ++w) { lb += redl[w]; nsel += redn[w]; }
   if (nsel == 0) lb = 0.f;
   const float smax = smax_ext ? smax_ext[row] : dec_max(ws.gmax[row]);
   if (smax_out && lane == 0) smax_out[row] = smax;
@@ -697,7 +697,7 @@ __global__ void __launch_bounds__(kThreads)
     if (e >= D) continue;
     float sb = 0.f;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) sb += red[w][e];
+    for (int w = 0; w < CW; ++w) sb += red[w][e];
     const float a = sb * fb + (hwn ? wp[2 + e] * fw : 0.f);
     if (out) {
       const float o = a / l;
