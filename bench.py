@@ -497,9 +497,9 @@ def main():
                 # per layer: window append + (single GPU) prep, scan, attend, combine, or
                 # (sharded) prep, scan, combine (local max), attend, combine (partial), merge
                 # + 2 exchanges (peer path; NCCL's own kernels not counted), or (fused
-                # peer path) prep, scan, attend, combine, allgather, merge
+                # peer path) prep, scan, attend, combine (pushes to peers), merge
                 "gpu_launches": a.steps * L * (5 if world == 1 else
-                                               {"p2p": 9, "p2p-fused": 7}.get(collective, 7)),
+                                               {"p2p": 9, "p2p-fused": 6}.get(collective, 7)),
                 "clocks": sampler.summary(), "parity": parity, "stats": stats,
                 "sharded_check": sharded_check,
                 "gen_seconds": round(t_gen, 2)}

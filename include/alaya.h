@@ -149,14 +149,27 @@ int alaya_attend(const alaya_params* p, const alaya_seq* seqs, int batch, const 
  * per-group flag to `epoch`; the attend kernel, running beside the scan, waits
  * for the n_ranks flags of each group it filters, takes the max over the
  * ranks' slots and filters at that global max - beta. Writes d_part as
- * alaya_attend does. Every rank calls it with the same epoch (the kind-0
+ * alaya_attend does (d_part may be NULL when gather_epoch != 0); gather_epoch
+ * != 0 also pushes the partials to every rank (see alaya_merge_exchanged), so
+ * the layer needs no separate collective. Every rank calls it with the same epoch (the kind-0
  * epoch counter of alaya_exch: slots of parity epoch&1, kind 0). A rank that
  * never arrives sets *d_err = 1 after a bounded poll. ALAYA_ERR_UNSUPPORTED
  * when the call is not tcgen05-eligible (use the staged path). */
 int alaya_sharded_step(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q,
                        void* const* bufs, int n_ranks, int rank, int64_t cap_floats,
-                       unsigned long long epoch, float* d_part, int* d_err, void* d_ws,
-                       size_t ws_bytes, void* stream);
+                       unsigned long long epoch, unsigned long long gather_epoch, float* d_part,
+                       int* d_err, void* d_ws, size_t ws_bytes, void* stream);
+
+/* Merge of the fused sharded step (replaces allgather -> merge of sharded.py;
+ * reference attention.py:128-152): with gather_epoch != 0, alaya_sharded_step's
+ * combine stores each row's partial straight into slot[rank] (kind 1) of every
+ * rank's buffer and the last row raises this rank's kind-1 flag everywhere; this
+ * kernel waits for the n_ranks flags of d_own_buf at `epoch` (= that
+ * gather_epoch, the kind-1 epoch counter of alaya_exch), merges the ranks'
+ * partials in rank order and finalizes to d_out [rows][dim]. Bounded poll:
+ * *d_err = 1 if a rank never arrives. */
+int alaya_merge_exchanged(void* d_own_buf, int n_ranks, int64_t cap_floats, unsigned long long epoch,
+                          int rows, int dim, float* d_out, int* d_status, int* d_err, void* stream);
 
 /* Stage 3: merge n_parts partial sets (d_parts: [n_parts][batch*Hq][dim+2]) in
  * order and finalize to d_out [batch*Hq][dim] fp32. Non-finite output sets

@@ -36,7 +36,7 @@ MAX_BATCH = 128
 # every symbol include/alaya.h declares (checked by tests/test_boundary.py)
 EXPORTS = (
     "alaya_last_error", "alaya_version", "alaya_workspace_bytes", "alaya_dipr_attention",
-    "alaya_scan", "alaya_attend", "alaya_sharded_step", "alaya_merge_partials", "alaya_merge_states", "alaya_selected",
+    "alaya_scan", "alaya_attend", "alaya_sharded_step", "alaya_merge_exchanged", "alaya_merge_partials", "alaya_merge_states", "alaya_selected",
     "alaya_ws_status", "alaya_window_append", "alaya_block_bounds", "alaya_ws_block_stats",
     "alaya_ws_candidate_counts", "alaya_topk", "alaya_block_reps", "alaya_block_topk",
     "alaya_sparse_attention", "alaya_avdb_stat", "alaya_avdb_write", "alaya_avdb_staging_bytes",
@@ -132,7 +132,10 @@ def load() -> ctypes.CDLL:
     lib.alaya_scan.argtypes = [P, S, i32, vp, vp, vp, sz, vp]
     lib.alaya_sharded_step.restype = i32
     lib.alaya_sharded_step.argtypes = [P, S, i32, vp, vp, i32, i32, ctypes.c_int64, ctypes.c_uint64,
-                                       vp, vp, vp, sz, vp]
+                                       ctypes.c_uint64, vp, vp, vp, sz, vp]
+    lib.alaya_merge_exchanged.restype = i32
+    lib.alaya_merge_exchanged.argtypes = [vp, i32, ctypes.c_int64, ctypes.c_uint64, i32, i32, vp, vp, vp,
+                                          vp]
     lib.alaya_attend.restype = i32
     lib.alaya_attend.argtypes = [P, S, i32, vp, vp, vp, i32, vp, sz, vp]
     lib.alaya_merge_partials.restype = i32

@@ -343,11 +343,14 @@ int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch
 
 int alaya_sharded_step(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q,
                        void* const* bufs, int n_ranks, int rank, int64_t cap_floats, unsigned long long epoch,
-                       float* d_part, int* d_err, void* d_ws, size_t ws_bytes, void* stream) {
+                       unsigned long long gather_epoch, float* d_part, int* d_err, void* d_ws,
+                       size_t ws_bytes, void* stream) {
   Call c;
   int rc = prepare(p, seqs, batch, d_ws, ws_bytes, stream, &c);
   if (rc) return rc;
-  if (!d_q || !d_part || !bufs) return fail(ALAYA_ERR_ARG, "null q/part/bufs");
+  if (!d_q || !bufs || (!d_part && !gather_epoch)) return fail(ALAYA_ERR_ARG, "null q/part/bufs");
+  if (gather_epoch && (int64_t)c.bt.B * c.bt.Hq * (p->dim + 2) > cap_floats)
+    return fail(ALAYA_ERR_SHAPE, "fused sharded step: partials beyond the exchange slot");
   if (n_ranks < 1 || n_ranks > kExMaxPeers || rank < 0 || rank >= n_ranks)
     return fail(ALAYA_ERR_ARG, "bad ranks %d/%d", rank, n_ranks);
   if (!c.use_tc) return fail(ALAYA_ERR_UNSUPPORTED, "fused sharded step needs the tcgen05 scan");
@@ -363,6 +366,7 @@ int alaya_sharded_step(const alaya_params* p, const alaya_seq* seqs, int batch, 
   c.bt.sx.R = n_ranks;
   c.bt.sx.cap = cap_floats;
   c.bt.sx.epoch = epoch;
+  c.bt.sx.gepoch = gather_epoch;
   c.bt.sx.err = d_err;
   if ((rc = run_scan(c, d_q))) return rc;
   if ((rc = c.st.attend_ovl(c.bt, d_q, c.ws, c.stream))) return rc;
@@ -400,6 +404,21 @@ int alaya_merge_partials(const float* d_parts, int n_parts, int rows, int dim, f
   if (rows == 0) return ALAYA_OK;
   merge_partials_kernel<<<rows, 128, 0, static_cast<cudaStream_t>(stream)>>>(
       d_parts, n_parts, rows, dim, d_out, nullptr, d_status);
+  return cuda_check("merge_partials_kernel");
+}
+
+int alaya_merge_exchanged(void* d_own_buf, int n_ranks, int64_t cap_floats, unsigned long long epoch, int rows,
+                          int dim, float* d_out, int* d_status, int* d_err, void* stream) {
+  if (!d_own_buf || !d_out || n_ranks < 1 || n_ranks > kExMaxPeers || rows < 0 || !dim_ok(dim) || epoch == 0)
+    return fail(ALAYA_ERR_ARG, "bad merge arguments");
+  if ((int64_t)rows * (dim + 2) > cap_floats) return fail(ALAYA_ERR_SHAPE, "partials beyond the exchange slot");
+  if (rows == 0) return ALAYA_OK;
+  char* buf = static_cast<char*>(d_own_buf);
+  const float* parts = reinterpret_cast<const float*>(buf + kExFlagBytes + (size_t)kExGroups * kExMaxPeers * 8) +
+                       ((size_t)(epoch & 1ull) * 2 + 1) * n_ranks * (size_t)cap_floats;
+  const unsigned long long* flags = reinterpret_cast<const unsigned long long*>(buf) + kExMaxPeers;  // kind 1
+  merge_partials_kernel<<<rows, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      parts, n_ranks, rows, dim, d_out, nullptr, d_status, flags, epoch, d_err, cap_floats);
   return cuda_check("merge_partials_kernel");
 }
 

@@ -48,8 +48,16 @@ struct ShardExch {
   int32_t rank, R;
   int64_t cap;                 // floats per slot
   unsigned long long epoch;    // this step's epoch (same on every rank)
+  unsigned long long gepoch;   // != 0: combine pushes the partials (allgather, kind 1) at this epoch
   int* err;                    // set to 1 when a rank never arrived (bounded poll)
 };
+// exchange head: [2 kinds][kExMaxPeers] u64 epoch flags, then the arrival counter (u64 index 32)
+__device__ __forceinline__ unsigned long long* exch_flag(char* buf, int kind, int r) {
+  return reinterpret_cast<unsigned long long*>(buf) + kind * kExMaxPeers + r;
+}
+__device__ __forceinline__ unsigned int* exch_arrive(char* buf) {
+  return reinterpret_cast<unsigned int*>(reinterpret_cast<unsigned long long*>(buf) + 2 * kExMaxPeers);
+}
 __device__ __forceinline__ float* exch_slot(char* buf, int parity, int kind, int r, int R, int64_t cap) {
   float* base = reinterpret_cast<float*>(buf + kExFlagBytes + (size_t)kExGroups * kExMaxPeers * 8);
   return base + ((((size_t)parity * 2 + kind) * R + r) * (size_t)cap);

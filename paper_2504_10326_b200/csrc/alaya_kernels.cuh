@@ -709,6 +709,29 @@ __global__ void __launch_bounds__(CW * 32)
       if (e == 0) { pr[0] = empty ? -INFINITY : m; pr[1] = empty ? 0.f : l; }
       pr[2 + e] = empty ? 0.f : a;
     }
+    if (bt.sx_on && bt.sx.gepoch) {  // fused allgather: the row straight into every rank's slot
+      const ShardExch& x = bt.sx;
+      const int parity = (int)(x.gepoch & 1ull);
+      for (int r = 0; r < x.R; ++r) {
+        float* pr = exch_slot(x.peers[r], parity, 1, x.rank, x.R, x.cap) + (size_t)row * (D + 2);
+        if (e == 0) { pr[0] = empty ? -INFINITY : m; pr[1] = empty ? 0.f : l; }
+        pr[2 + e] = empty ? 0.f : a;
+      }
+    }
+  }
+  if (bt.sx_on && bt.sx.gepoch) {  // last row out raises this rank's kind-1 flag everywhere
+    const ShardExch& x = bt.sx;
+    __threadfence_system();
+    __syncwarp();
+    unsigned int last = 0;
+    if (lane == 0) last = atomicAdd(exch_arrive(x.peers[x.rank]), 1u) == gridDim.x - 1;
+    last = __shfl_sync(kFull, last, 0);
+    if (last) {
+      if (lane == 0) *exch_arrive(x.peers[x.rank]) = 0u;  // the next exchange starts after this kernel
+      __threadfence_system();
+      __syncwarp();
+      if (lane < x.R) st_release_sys_u64(exch_flag(x.peers[lane], 1, x.rank), x.gepoch);
+    }
   }
 }
 

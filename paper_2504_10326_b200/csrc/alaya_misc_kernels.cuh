@@ -9,21 +9,43 @@ namespace alaya {
 // Merge of shard partials (attention.py:128-152), rows = batch * Hq.
 __global__ void merge_partials_kernel(const float* __restrict__ parts, int n_parts, int rows, int D,
                                       float* __restrict__ out, float* __restrict__ state_out,
-                                      int* status) {
+                                      int* status, const unsigned long long* flags = nullptr,
+                                      unsigned long long epoch = 0, int* err = nullptr,
+                                      int64_t part_stride = 0) {
   const int row = blockIdx.x;
-  const size_t stride = (size_t)rows * (D + 2);
+  if (flags) {  // parts are the exchange slots the ranks push into (fused sharded step): wait for them
+    __shared__ int s_bad;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    if (threadIdx.x < n_parts) {
+      long long polls = 0;
+      while (ld_acquire_sys_u64(flags + threadIdx.x) < epoch) {
+        if (++polls > (1ll << 26)) {
+          s_bad = 1;
+          break;
+        }
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+    if (s_bad) {
+      if (threadIdx.x == 0 && err) atomicExch(err, 1);
+      return;
+    }
+  }
+  const size_t stride = part_stride ? (size_t)part_stride : (size_t)rows * (D + 2);
   float m = -INFINITY;
-  for (int r = 0; r < n_parts; ++r) m = fmaxf(m, parts[r * stride + (size_t)row * (D + 2)]);
+  for (int r = 0; r < n_parts; ++r) m = fmaxf(m, __ldcg(parts + r * stride + (size_t)row * (D + 2)));
   float l = 0.f;
   for (int r = 0; r < n_parts; ++r) {
     const float* p = parts + r * stride + (size_t)row * (D + 2);
-    if (p[0] != -INFINITY) l += p[1] * expf(p[0] - m);
+    if (__ldcg(p) != -INFINITY) l += __ldcg(p + 1) * expf(__ldcg(p) - m);
   }
   for (int e = threadIdx.x; e < D; e += blockDim.x) {
     float a = 0.f;
     for (int r = 0; r < n_parts; ++r) {
       const float* p = parts + r * stride + (size_t)row * (D + 2);
-      if (p[0] != -INFINITY) a += p[2 + e] * expf(p[0] - m);
+      if (__ldcg(p) != -INFINITY) a += __ldcg(p + 2 + e) * expf(__ldcg(p) - m);
     }
     if (out) {
       const float o = a / l;

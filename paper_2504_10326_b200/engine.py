@@ -221,22 +221,26 @@ class Call:
         return part
 
     def sharded_step(self, q: torch.Tensor, bufs, n_ranks: int, rank: int, cap: int, epoch: int,
-                     err: torch.Tensor) -> torch.Tensor | None:
+                     err: torch.Tensor, gather_epoch: int = 0) -> torch.Tensor | bool | None:
         """Scan + global max over peer memory + attend in one launch sequence
         (``alaya_sharded_step``): ``[B*Hq, dim+2]`` partials filtered at the global
-        max, or ``None`` when the call is not eligible (staged path instead)."""
+        max, or (``gather_epoch``) ``True`` once the partials were pushed to every
+        rank's exchange slots; ``None`` when the call is not eligible."""
         q = self._q(q)
-        part = torch.empty(self.B * self.params.n_query_heads, self.params.dim + 2,
-                           dtype=torch.float32, device=self.device)
+        part = None
+        if not gather_epoch:
+            part = torch.empty(self.B * self.params.n_query_heads, self.params.dim + 2,
+                               dtype=torch.float32, device=self.device)
         rc = self.lib.alaya_sharded_step(ctypes.byref(self.params), self.seqs, self.B, q.data_ptr(),
-                                         bufs, n_ranks, rank, cap, epoch, part.data_ptr(),
+                                         bufs, n_ranks, rank, cap, epoch, gather_epoch,
+                                         part.data_ptr() if part is not None else None,
                                          err.data_ptr(), self.ws.data_ptr(), self.ws_bytes,
                                          self.stream)
         if rc == 6:  # ALAYA_ERR_UNSUPPORTED
             return None
         check(rc)
         self._q_keep = q
-        return part
+        return part if part is not None else True
 
     def topk(self, q: torch.Tensor, k: int, with_scores: bool = False):
         """Exact flat top-k per (seq, q head) (``FlatIndex.top_k``, ``index.py:60-66``):

@@ -72,19 +72,27 @@ class EngineStages:
     def merge(self, parts):
         return engine.merge_partials(parts, self.dim)
 
-    def fused(self, q, exchange: "PeerExchange"):
+    def fused(self, q, exchange: "PeerExchange", gather: bool = False):
         """Scan -> max over peers -> attend as one launch sequence (the max
         travels over NVLink per (seq, kv head) group as the scan completes it).
-        ``None`` when not eligible."""
-        if q.shape[0] * q.shape[1] > exchange.cap:
+        Returns the local partials, or with ``gather`` the merged output
+        ``[B*Hq, d]`` (the combine pushes the partials to every rank, the merge
+        waits for the ranks' flags: no collective kernel at all). ``None`` when
+        not eligible."""
+        rows = q.shape[0] * q.shape[1]
+        if rows > exchange.cap or (gather and rows * (self.dim + 2) > exchange.cap):
             return None
-        e = exchange.epoch[0] + 1
+        e, ge = exchange.epoch[0] + 1, (exchange.epoch[1] + 1 if gather else 0)
         part = self.call.sharded_step(q, exchange._arr, exchange.world, exchange.rank, exchange.cap,
-                                      e, exchange.err)
-        if part is not None:
-            exchange.epoch[0] = e
+                                      e, exchange.err, ge)
         self.fused_used = part is not None
-        return part
+        if part is None:
+            return None
+        exchange.epoch[0] = e
+        if not gather:
+            return part
+        exchange.epoch[1] = ge
+        return exchange.merge_exchanged(rows, self.dim, ge)
 
 
 def _staged(t: torch.Tensor, group) -> tuple[torch.Tensor, bool]:
@@ -176,6 +184,16 @@ class PeerExchange:
         flat = _tensor_at(ptr, self.world * self.cap, self.device)
         return flat.view(self.world, self.cap)[:, :n].reshape((self.world,) + tuple(local.shape))
 
+    def merge_exchanged(self, rows: int, dim: int, epoch: int) -> torch.Tensor:
+        """Wait for every rank's kind-1 flag at ``epoch`` and merge the pushed
+        partials (``alaya_merge_exchanged``) -> ``[rows, dim]``."""
+        from . import _lib
+        out = torch.empty(rows, dim, dtype=torch.float32, device=self.device)
+        _lib.check(_lib.load().alaya_merge_exchanged(
+            self.own, self.world, self.cap, epoch, rows, dim, out.data_ptr(), None,
+            self.err.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream))
+        return out
+
     def check(self) -> None:
         if int(self.err.item()):
             raise RuntimeError("peer exchange timed out: a rank never arrived")
@@ -206,13 +224,16 @@ def sharded_attention(stages: LocalStages, q: torch.Tensor, group=None,
                       exchange: PeerExchange | None = None) -> torch.Tensor:
     """One decode step of one layer over sequence-sharded KV -> ``[B, Hq, d]``
     (identical on every rank). With ``exchange`` the two collectives run over
-    peer memory (``alaya_exch``), otherwise through ``torch.distributed``."""
+    peer memory: fused into the kernels (``alaya_sharded_step`` +
+    ``alaya_merge_exchanged``) when the call is tcgen05-eligible, else as
+    ``alaya_exch`` kernels; without, through ``torch.distributed``."""
     if exchange is not None:
         fused = getattr(stages, "fused", None) if exchange.fused else None
-        part = fused(q, exchange) if fused is not None else None
-        if part is None:
-            smax = exchange.allreduce_max(stages.scan(q))
-            part = stages.attend(q, smax).contiguous()
+        out = fused(q, exchange, gather=True) if fused is not None else None
+        if out is not None:
+            return out.view(q.shape[0], q.shape[1], -1)
+        smax = exchange.allreduce_max(stages.scan(q))
+        part = stages.attend(q, smax).contiguous()
         parts = exchange.allgather(part)
         out = stages.merge(parts)
         return out.view(q.shape[0], q.shape[1], -1)

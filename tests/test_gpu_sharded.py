@@ -181,20 +181,23 @@ def test_sharded_attention_over_peer_exchange(cuda_ok):
         _lib.load().alaya_exch_free(b)
 
 
-def test_fused_sharded_step_emulated(cuda_ok):
+@pytest.mark.parametrize("world,lens", [(2, (6000, 7000)), (3, (2, 9000)), (4, (5000, 1))])
+def test_fused_sharded_step_emulated(cuda_ok, world, lens):
     """alaya_sharded_step (scan -> per-group max over peer memory -> attend) for
-    2 ranks emulated on streams of one GPU at a size whose grids co-reside (each
-    rank's attend waits on the other's scan: the bounded poll turns a missed
-    arrival into the error flag, not a hang), vs the unsharded kernels."""
+    2-4 ranks emulated on streams of one GPU at a size whose grids co-reside
+    (each rank's attend waits on the others' scans: the bounded poll turns a
+    missed arrival into the error flag, not a hang), vs the unsharded kernels.
+    Sequences shorter than the world leave shards with no tokens of them: those
+    ranks export -inf maxima from prep_kernel."""
     from paper_2504_10326_b200 import _lib, engine
     from paper_2504_10326_b200.sharded import EngineStages, local_view
     dev = torch.device("cuda")
-    world, B, hkv, g, d, n, w, beta = 2, 2, 2, 4, 128, 6000, 3, 5.0
+    B, hkv, g, d, w, beta = len(lens), 2, 4, 128, 3, 5.0
     dtype = torch.bfloat16
-    r = np.random.default_rng(9)
+    r = np.random.default_rng(9 + world)
     K, V, WK, WV, qs = [], [], [], [], []
     for b in range(B):
-        _, k, v, centers, _ = O.make_context(n + 1000 * b, 1, hkv, d, seed=700 + b)
+        _, k, v, centers, _ = O.make_context(lens[b], 1, hkv, d, seed=700 + b)
         K.append(torch.from_numpy(O.bf16_round(k)[0]).to(dev, dtype))
         V.append(torch.from_numpy(O.bf16_round(v)[0]).to(dev, dtype))
         WK.append(torch.randn(hkv, w, d, device=dev).to(dtype))
@@ -213,21 +216,35 @@ def test_fused_sharded_step_emulated(cuda_ok):
     exs, bufs = _exchange_group(world, B * hkv * g * (d + 2), dev)
     streams = [torch.cuda.Stream() for _ in range(world)]
     torch.cuda.synchronize()
-    for _ in range(3):
+    rows = q.shape[0] * q.shape[1]
+    for it in range(4):
         parts, outs = [None] * world, [None] * world
-        for rk in range(world):
-            with torch.cuda.stream(streams[rk]):
-                parts[rk] = stages[rk].fused(q, exs[rk])
-                assert parts[rk] is not None and stages[rk].fused_used
-        for rk in range(world):
-            with torch.cuda.stream(streams[rk]):
-                parts[rk] = exs[rk].allgather(parts[rk])
-        for rk in range(world):
-            with torch.cuda.stream(streams[rk]):
-                outs[rk] = stages[rk].merge(parts[rk]).view(q.shape[0], q.shape[1], -1)
+        if it % 2 == 0:  # fused scan/max/attend, then the alaya_exch allgather + merge
+            for rk in range(world):
+                with torch.cuda.stream(streams[rk]):
+                    parts[rk] = stages[rk].fused(q, exs[rk])
+                    assert parts[rk] is not None and stages[rk].fused_used
+            for rk in range(world):
+                with torch.cuda.stream(streams[rk]):
+                    parts[rk] = exs[rk].allgather(parts[rk])
+            for rk in range(world):
+                with torch.cuda.stream(streams[rk]):
+                    outs[rk] = stages[rk].merge(parts[rk])
+        else:  # fully fused: the combine pushes the partials, the merge waits for the flags
+            ge = exs[0].epoch[1] + 1
+            for rk in range(world):
+                with torch.cuda.stream(streams[rk]):
+                    e = exs[rk].epoch[0] + 1
+                    assert stages[rk].call.sharded_step(q, exs[rk]._arr, world, rk, exs[rk].cap, e,
+                                                        exs[rk].err, ge) is True
+                    exs[rk].epoch[0], exs[rk].epoch[1] = e, ge
+            for rk in range(world):
+                with torch.cuda.stream(streams[rk]):
+                    outs[rk] = exs[rk].merge_exchanged(rows, d, ge)
         torch.cuda.synchronize()
         for rk in range(world):
             exs[rk].check()
-            assert float(((outs[rk] - o_full).norm() / o_full.norm()).item()) <= 2e-6
+            o = outs[rk].view(q.shape[0], q.shape[1], -1)
+            assert float(((o - o_full).norm() / o_full.norm()).item()) <= 2e-6, (it, rk)
     for b in bufs:
         _lib.load().alaya_exch_free(b)
