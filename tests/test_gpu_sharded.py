@@ -248,3 +248,24 @@ def test_fused_sharded_step_emulated(cuda_ok, world, lens):
             assert float(((o - o_full).norm() / o_full.norm()).item()) <= 2e-6, (it, rk)
     for b in bufs:
         _lib.load().alaya_exch_free(b)
+
+
+def test_fused_sharded_step_falls_back_when_ineligible(cuda_ok):
+    """fp32 K/V (CUDA-core scan): alaya_sharded_step answers UNSUPPORTED, the
+    stage reports it (None) and sharded_attention takes the staged peer path."""
+    from paper_2504_10326_b200 import _lib, engine
+    from paper_2504_10326_b200.sharded import EngineStages, local_view
+    dev = torch.device("cuda")
+    world, hkv, g, d, n = 2, 2, 4, 128, 3000
+    _, k, v, centers, _ = O.make_context(n, 1, hkv, d, seed=41)
+    K = torch.from_numpy(k[0]).to(dev)
+    V = torch.from_numpy(v[0]).to(dev)
+    params = engine.make_params(hkv * g, hkv, d, torch.float32, 5.0, 16, 64)
+    q = torch.tensor(centers[:hkv * g][None], dtype=torch.float32, device=dev)
+    st = EngineStages([local_view(K, V, world, 0)], params, torch.float32, dev)
+    exs, bufs = _exchange_group(world, hkv * g * (d + 2), dev)
+    assert st.fused(q, exs[0]) is None and not st.fused_used
+    assert st.fused(q, exs[0], gather=True) is None
+    assert exs[0].epoch == [0, 0]  # nothing was consumed
+    for b in bufs:
+        _lib.load().alaya_exch_free(b)
