@@ -1,5 +1,6 @@
 // C-ABI entry points (include/alaya.h): validation, workspace layout, kernel
 // dispatch over (dtype, dim, group size) and launch.
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdlib>
@@ -136,7 +137,7 @@ size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 struct Layout {
   size_t zero_bytes;
   size_t cscore_end;
-  size_t status, gmax, counters, cnt, selcnt, retcnt, part_l, part_acc, cidx, cscore, partbuf, smaxbuf,
+  size_t status, seeded, gmax, counters, cnt, selcnt, retcnt, part_l, part_acc, cidx, cscore, partbuf, smaxbuf,
       keep, ovl_l, ovl_acc, ovl_sel, ovl_ret, heavy, ovlist, total;
 };
 
@@ -144,7 +145,8 @@ Layout layout_for(const Batch& bt) {
   Layout L;
   const size_t C = (size_t)bt.total_chunks, G = bt.G, D = bt.D, rows = (size_t)bt.B * bt.Hq;
   size_t o = 0;
-  L.status = o; o = align_up(o + 4);
+  L.status = o; o = align_up(o + 16);  // status, ready
+  L.seeded = o; o = align_up(o + 8 * (size_t)bt.B * bt.Hkv);
   L.gmax = o; L.counters = o + 4 * rows;
   L.zero_bytes = 4 * rows + 64 + 4 * (size_t)bt.B * bt.Hkv;  // gmax, counters, group_done (prep_kernel)
   o = align_up(o + L.zero_bytes);
@@ -173,6 +175,8 @@ Ws carve(const Layout& L, void* base) {
   char* c = static_cast<char*>(base);
   Ws w;
   w.status = reinterpret_cast<int*>(c + L.status);
+  w.ready = reinterpret_cast<unsigned long long*>(c + L.status + 8);
+  w.seeded = reinterpret_cast<unsigned long long*>(c + L.seeded);
   w.gmax = reinterpret_cast<uint32_t*>(c + L.gmax);
   w.counters = reinterpret_cast<int*>(c + L.counters);
   w.group_done = w.counters + 16;
@@ -236,9 +240,17 @@ int prepare(const alaya_params* p, const alaya_seq* seqs, int B, void* d_ws, siz
   return ALAYA_OK;
 }
 
-int run_scan(Call& c, const float* d_q) {
-  const size_t rows = (size_t)c.bt.B * c.bt.Hq;
-  (void)rows;
+int run_scan(Call& c, const float* d_q, bool ends_in_combine = true) {
+  // the tcgen05 scan starts on prep's zeroed header (ws.ready) instead of prep's
+  // completion; the seeds land by atomicMax while it runs (ALAYA_PREP_ASYNC=0: off)
+  static const int async_prep = [] {
+    const char* v = getenv("ALAYA_PREP_ASYNC");
+    return v && *v ? atoi(v) : 1;
+  }();
+  static std::atomic<unsigned long long> next_id{1};
+  // (the call's combine_kernel waits for prep's last seed, so none lands in a later call)
+  c.bt.call_id =
+      (async_prep && ends_in_combine && c.use_tc && !c.bt.block_filter && !c.bt.topk_thr) ? next_id++ : 0ull;
   int rc = c.st.prep(c.bt, d_q, c.ws, c.stream);  // zeroes the header, seeds the max
   if (rc) return rc;
   if (c.bt.block_filter) {
@@ -379,7 +391,7 @@ int alaya_scan(const alaya_params* p, const alaya_seq* seqs, int batch, const fl
   int rc = prepare(p, seqs, batch, d_ws, ws_bytes, stream, &c);
   if (rc) return rc;
   if (!d_q) return fail(ALAYA_ERR_ARG, "null q");
-  if ((rc = run_scan(c, d_q))) return rc;
+  if ((rc = run_scan(c, d_q, d_smax != nullptr))) return rc;
   if (!d_smax) return ALAYA_OK;  // scan only (kernel timing)
   // export the local max (decoded); combine with no outputs does only that
   return c.st.combine(c.bt, nullptr, c.ws, nullptr, nullptr, d_smax, c.stream);

@@ -84,6 +84,8 @@ struct Batch {
   int32_t dbg;  // diagnostics only (ALAYA_TC_DBG): bit0 no L2 hint, bit1 no epilogue math, bit2 no MMA
   int32_t block_filter;
   int32_t split;  // attend task split threshold (candidates per (chunk, head) pair)
+  unsigned long long call_id;  // != 0: prep publishes the zeroed header as ws.ready = call_id and
+                               // seeds asynchronously (the tcgen05 scan waits on ready, not on prep)
   int32_t seed;   // prep_kernel seeds the running max from sampled keys
   int32_t overlap;  // scan publishes per-group completion; attend runs beside it (PDL)
   const float* topk_thr;  // TOP_K: per-row candidate threshold (a lower bound of the k-th
@@ -100,10 +102,12 @@ struct BixSet {
 // Workspace pointers (device), carved from the caller's buffer.
 struct Ws {
   int* status;
+  unsigned long long* ready;  // call id whose header prep has zeroed (next to status, never zeroed)
+  unsigned long long* seeded;  // [B*Hkv] call id whose seeds of (seq, kv head) are in gmax (never zeroed)
   uint32_t* gmax;   // [B*Hq] order-preserving encoded running max
   int* counters;    // [16] right after gmax (zeroed by prep_kernel): [0] attend ticket,
                     // [2..3] block-filter kept/total, [6] epilogue-warp chunk publications
-                    // (overlapped attend), [7] overflow items
+                    // (overlapped attend), [7] overflow items, [8] prep CTAs done seeding
   int* group_done;  // [B*Hkv] right after counters: chunk publications per (seq, kv head)
   int* cnt;         // [chunks*G*4] candidate counts per scan sub-list (see CandList)
   int* selcnt;      // [chunks*G]
@@ -131,6 +135,11 @@ struct Ws {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

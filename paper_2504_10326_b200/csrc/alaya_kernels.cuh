@@ -618,6 +618,8 @@ __global__ void __launch_bounds__(CW * 32)
   __shared__ int redn[CW];
   pdl_trigger();
   pdl_wait();
+  if (bt.call_id && threadIdx.x == 0)  // this call's prep has finished (async seeds)
+    while (ld_acquire_gpu(&ws.counters[8]) < bt.B * bt.Hkv) __nanosleep(64);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int row = blockIdx.x;
   const int b = row / bt.Hq, qh = row - b * bt.Hq;
@@ -775,11 +777,26 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.x / bt.Hkv, h = blockIdx.x - b * bt.Hkv;
   const KSeq& s = bt.s[b];
-  if (blockIdx.x == 0 && threadIdx.x < 16) {
-    ws.counters[threadIdx.x] = 0;
-    if (threadIdx.x == 0) *ws.status = 0;
+  const bool async = bt.call_id != 0;
+  if (async) {  // CTA 0 zeroes the whole header, then publishes it (the scan waits on ws.ready)
+    if (blockIdx.x == 0) {
+      const int rows = bt.B * bt.Hq;
+      for (int i = threadIdx.x; i < rows; i += blockDim.x) ws.gmax[i] = 0u;
+      for (int i = threadIdx.x; i < bt.B * bt.Hkv; i += blockDim.x) ws.group_done[i] = 0;
+      if (threadIdx.x < 16) ws.counters[threadIdx.x] = 0;
+      if (threadIdx.x == 0) *ws.status = 0;
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0)
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ws.ready), "l"(bt.call_id) : "memory");
+    }
+  } else {
+    if (blockIdx.x == 0 && threadIdx.x < 16) {
+      ws.counters[threadIdx.x] = 0;
+      if (threadIdx.x == 0) *ws.status = 0;
+    }
+    if (threadIdx.x == 0) ws.group_done[blockIdx.x] = 0;
   }
-  if (threadIdx.x == 0) ws.group_done[blockIdx.x] = 0;
   if (bt.sx_on && s.nch == 0) {  // fused sharded step: no chunk will complete this group
     const ShardExch& x = bt.sx;
     const int parity = (int)(x.epoch & 1ull);
@@ -815,7 +832,7 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
   const int na = (int)(a1 - a0), nbw = (int)(b1 - b0);
   // window rows join the sample only when the block filter consumes the seed (they
   // tighten its LB; otherwise the extra load rounds cost more than they save)
-  const int R = S + (bt.block_filter ? min(na + nbw, 2 * kPrepSamples) : 0);
+  const int R = bt.seed ? S + (bt.block_filter ? min(na + nbw, 2 * kPrepSamples) : 0) : 0;
   constexpr int RU = kPrepSamples / kWarps;  // rows in flight per warp
   for (int i0 = warp * RU; i0 < R; i0 += kWarps * RU) {
     float x[RU][DL];
@@ -853,6 +870,29 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
 #pragma unroll
     for (int j = 0; j < G; ++j) red[warp][j] = best[j];
   __syncthreads();
+  if (async) {  // seeds join the running max once the header is zeroed; then count this CTA done
+    __shared__ int s_ok;
+    if (threadIdx.x == 0) {
+      // bounded: a seed is optional (a lower bound), so a CTA that cannot see the
+      // header published (CTA 0 not resident) drops its seed instead of spinning on
+      int polls = 0;
+      while (ld_acquire_gpu_u64(ws.ready) != bt.call_id && ++polls < (1 << 20)) __nanosleep(32);
+      s_ok = polls < (1 << 20);
+    }
+    __syncthreads();
+    if (s_ok && threadIdx.x < G) {
+      float m = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) m = fmaxf(m, red[w][threadIdx.x]);
+      if (bt.seed && m > -INFINITY) atomicMax(&ws.gmax[b * bt.Hq + h * G + threadIdx.x], enc_max(m));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ws.seeded + blockIdx.x), "l"(bt.call_id) : "memory");
+      asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(&ws.counters[8]), "r"(1) : "memory");
+    }
+    return;
+  }
   if (threadIdx.x < G) {
     float m = -INFINITY;
 #pragma unroll

@@ -312,7 +312,13 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 4 : (kStages <= 3 
   // the preceding kernels) steer it. Every other warp waits (q, gmax seeds,
   // tickets), then triggers: a dependent launched after the trigger sees all
   // earlier work complete.
-  if (warp != 0 || bt.block_filter) pdl_wait();
+  if (warp != 0 && bt.call_id) {  // async prep: the zeroed header is published as ws.ready
+    if (lane == 0)
+      while (ld_acquire_gpu_u64(ws.ready) != bt.call_id) __nanosleep(32);
+    __syncwarp();
+  } else if (warp != 0 || bt.block_filter) {
+    pdl_wait();
+  }
   if (warp != 0) pdl_trigger();
 
   if (warp == 0) {
@@ -411,7 +417,19 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 4 : (kStages <= 3 
 #pragma unroll
       for (int j = 0; j < G; ++j) pre[j] = __ldcg(&ws.gmax[b * bt.Hq + h * G + j]);
     };
-    if (blockIdx.x < bt.total_chunks) load_pre(blockIdx.x);
+    if (blockIdx.x < bt.total_chunks) {
+      if (bt.call_id) {  // async prep: the first chunk starts from its group's seed (bounded wait)
+        int b, h, ci;
+        decode_chunk(bt, blockIdx.x, b, h, ci);
+        if (lane == 0) {
+          int polls = 0;
+          while (ld_acquire_gpu_u64(ws.seeded + b * bt.Hkv + h) != bt.call_id && ++polls < (1 << 20))
+            __nanosleep(32);
+        }
+        __syncwarp();
+      }
+      load_pre(blockIdx.x);
+    }
     for (int c = blockIdx.x; c < bt.total_chunks; c += gridDim.x) {
       uint32_t cur[G];
 #pragma unroll
