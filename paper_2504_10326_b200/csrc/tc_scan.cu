@@ -128,7 +128,10 @@ bool pdl_enabled() {
 // sessions of 8 kv heads, neutral to -1% at 1-2 sessions)
 bool overlap_enabled(int groups) {
   static const int mode = env_int("ALAYA_OVERLAP", -1);
-  return mode > 0 || (mode < 0 && groups >= 32);
+  // on by default since the async prep / combine changes (v16): B=1 89.0 -> 86.1 us,
+  // B=2 132.7 -> 129.0, 8K ctx B=4 55.9 -> 51.6 (tools/probe_latency.py)
+  (void)groups;
+  return mode != 0;
 }
 
 int launch_tc_scan(const Batch& bt_in, const alaya_seq* seqs, const float* q, const Ws& ws,
