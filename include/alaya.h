@@ -81,6 +81,12 @@ typedef struct {
    * params.block_filter == 0. */
   const void* bounds;
   int64_t bounds_head_stride;
+  /* Optional DEVICE window row count (CUDA-graph mode). When non-NULL the kernels
+   * read the session-window row count from *d_w when they run, `w` is the ring
+   * CAPACITY in rows, and alaya_window_append writes row *d_w and increments it
+   * (rows beyond the capacity are dropped). A decode step captured once as a
+   * CUDA graph then stays valid while the window grows. NULL: `w` is the count. */
+  int32_t* d_w;
 } alaya_seq;
 
 typedef struct {

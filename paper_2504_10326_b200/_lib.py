@@ -56,6 +56,7 @@ class AlayaSeq(ctypes.Structure):
         ("token_offset", ctypes.c_int64), ("prefix_len", ctypes.c_int64),
         ("n", ctypes.c_int32), ("w", ctypes.c_int32),
         ("bounds", ctypes.c_void_p), ("bounds_head_stride", ctypes.c_int64),
+        ("d_w", ctypes.c_void_p),
     ]
 
 

@@ -121,7 +121,7 @@ int build_batch(const alaya_params* p, const alaya_seq* seqs, int B, Batch* bt) 
     k.k = s.k; k.v = s.v; k.wk = s.wk; k.wv = s.wv;
     k.hs = s.head_stride; k.whs = s.w_head_stride;
     k.off = s.token_offset; k.P = s.prefix_len;
-    k.n = s.n; k.w = s.w;
+    k.n = s.n; k.w = s.w; k.dw = s.d_w;
     k.nch = (s.n + chunk - 1) / chunk;
     k.bnd = s.bounds;
     k.bhs = s.bounds_head_stride;
@@ -249,8 +249,13 @@ int run_scan(Call& c, const float* d_q, bool ends_in_combine = true) {
   }();
   static std::atomic<unsigned long long> next_id{1};
   // (the call's combine_kernel waits for prep's last seed, so none lands in a later call)
-  c.bt.call_id =
-      (async_prep && ends_in_combine && c.use_tc && !c.bt.block_filter && !c.bt.topk_thr) ? next_id++ : 0ull;
+  // (not inside a CUDA-graph capture: every replay would reuse the captured id)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(c.stream, &cap) != cudaSuccess) cap = cudaStreamCaptureStatusActive;
+  c.bt.call_id = (async_prep && ends_in_combine && c.use_tc && !c.bt.block_filter && !c.bt.topk_thr &&
+                  cap == cudaStreamCaptureStatusNone)
+                     ? next_id++
+                     : 0ull;
   int rc = c.st.prep(c.bt, d_q, c.ws, c.stream);  // zeroes the header, seeds the max
   if (rc) return rc;
   if (c.bt.block_filter) {
@@ -318,18 +323,24 @@ int alaya_window_append(const alaya_params* p, const alaya_seq* seqs, int batch,
   int rc = build_batch(p, seqs, batch, &bt);
   if (rc) return rc;
   if (!d_k || !d_v) return fail(ALAYA_ERR_ARG, "null k/v");
+  bool dev_w = false;
   for (int b = 0; b < batch; ++b) {
     if (!seqs[b].wk || !seqs[b].wv) return fail(ALAYA_ERR_ARG, "seq %d: null window buffers", b);
-    if (seqs[b].w_head_stride < (int64_t)(seqs[b].w + 1) * p->dim)
+    // host count: row w must fit; device count (d_w): w is the capacity, checked in the kernel
+    const int64_t rows = seqs[b].d_w ? seqs[b].w : (int64_t)seqs[b].w + 1;
+    if (seqs[b].w_head_stride < rows * p->dim)
       return fail(ALAYA_ERR_SHAPE, "seq %d: window row %d beyond capacity", b, seqs[b].w);
+    dev_w = dev_w || seqs[b].d_w;
   }
   const long total = (long)batch * p->n_kv_heads * p->dim;
   const int blocks = (int)std::min<long>((total + 255) / 256, 1024);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (p->dtype == ALAYA_BF16)
-    return launch_pdl("window_append_kernel", window_append_kernel<__nv_bfloat16>, blocks, 256, 0, st, bt, d_k,
-                      d_v);
-  return launch_pdl("window_append_kernel", window_append_kernel<float>, blocks, 256, 0, st, bt, d_k, d_v);
+  rc = p->dtype == ALAYA_BF16
+           ? launch_pdl("window_append_kernel", window_append_kernel<__nv_bfloat16>, blocks, 256, 0, st, bt,
+                        d_k, d_v)
+           : launch_pdl("window_append_kernel", window_append_kernel<float>, blocks, 256, 0, st, bt, d_k, d_v);
+  if (rc || !dev_w) return rc;
+  return launch_pdl("window_commit_kernel", window_commit_kernel, 1, 128, 0, st, bt);  // ++*d_w
 }
 
 int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q,

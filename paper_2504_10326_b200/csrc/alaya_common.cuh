@@ -33,7 +33,10 @@ struct KSeq {
   int32_t nch;         // chunks per kv head
   const void* bnd;     // block bounds [Hkv][bhs] ([block][2][D]) or null
   int64_t bhs;
+  int* dw;             // device window row count (graph mode; w = capacity) or null
 };
+// session-window rows of a sequence at kernel run time
+__device__ __forceinline__ int seq_w(const KSeq& s) { return s.dw ? min(__ldcg(s.dw), s.w) : s.w; }
 
 // Sequence-sharded step with the collectives fused into the kernels (peer
 // memory): the tcgen05 scan's CTA that completes a (sequence, kv head) group

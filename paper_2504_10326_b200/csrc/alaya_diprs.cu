@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
     int64_t a1, b0, b1;
     if (P <= (int64_t)bt.wi + bt.wl) { a1 = P; b0 = 0; b1 = 0; }
     else { a1 = bt.wi; b0 = P - bt.wl; b1 = P; }
-    const int na = (int)a1, nbw = (int)(b1 - b0), R = na + nbw + s.w;
+    const int na = (int)a1, nbw = (int)(b1 - b0), R = na + nbw + seq_w(s);
     const T* wkb = reinterpret_cast<const T*>(s.wk) + (size_t)h * s.whs;
     float m = -INFINITY;
     for (int r = hw; r < ((R + 1) & ~1); r += kDThreads / 16) {  // pairs of rows per warp

@@ -400,7 +400,7 @@ __device__ __forceinline__ void win_task(const Batch& bt, const float* __restric
   a0 = max(a0, off) - off; a1 = min(a1, off + s.n) - off; if (a1 < a0) a1 = a0;
   b0 = max(b0, off) - off; b1 = min(b1, off + s.n) - off; if (b1 < b0) b1 = b0;
   const int na = (int)(a1 - a0), nbw = (int)(b1 - b0);
-  const int R = na + nbw + s.w;
+  const int R = na + nbw + seq_w(s);
   const T* kbase = reinterpret_cast<const T*>(s.k) + (size_t)h * s.hs;
   const T* vbase = reinterpret_cast<const T*>(s.v) + (size_t)h * s.hs;
   const T* wkb = reinterpret_cast<const T*>(s.wk) + (size_t)h * s.whs;

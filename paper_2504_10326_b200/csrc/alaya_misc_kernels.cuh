@@ -60,6 +60,16 @@ __global__ void merge_partials_kernel(const float* __restrict__ parts, int n_par
   }
 }
 
+// Graph mode: commit the appended window row (after every append thread read *dw).
+__global__ void window_commit_kernel(const __grid_constant__ Batch bt) {
+  pdl_wait();
+  pdl_trigger();
+  for (int b = threadIdx.x; b < bt.B; b += blockDim.x) {
+    const KSeq& s = bt.s[b];
+    if (s.dw && *s.dw < s.w) *s.dw += 1;
+  }
+}
+
 // Selected ids (global, ascending) + counts per (sequence, q head).
 __global__ void selected_kernel(const __grid_constant__ Batch bt, Ws ws, int64_t* __restrict__ ids,
                                 int64_t cap, int32_t* __restrict__ nsel, int32_t* __restrict__ nret) {
@@ -97,7 +107,9 @@ __global__ void window_append_kernel(const __grid_constant__ Batch bt, const flo
     const long bh = i / D;
     const int h = (int)(bh % bt.Hkv), b = (int)(bh / bt.Hkv);
     const KSeq& s = bt.s[b];
-    const size_t off = (size_t)h * s.whs + (size_t)s.w * D + e;
+    const int row = s.dw ? __ldcg(s.dw) : s.w;
+    if (s.dw && row >= s.w) continue;  // ring full (graph mode): dropped, not committed
+    const size_t off = (size_t)h * s.whs + (size_t)row * D + e;
     T* wk = const_cast<T*>(reinterpret_cast<const T*>(s.wk));
     T* wv = const_cast<T*>(reinterpret_cast<const T*>(s.wv));
     if constexpr (std::is_same_v<T, float>) {

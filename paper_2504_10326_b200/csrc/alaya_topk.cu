@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(kSaWarps * 32)
   const int na = (int)(a1 - a0), nbw = (int)(b1 - b0);
   const int nid = count[row];
   const int64_t* rid = ids + (size_t)row * cap;
-  const int R = nid + na + nbw + s.w;  // id rows first, then the window rows
+  const int R = nid + na + nbw + seq_w(s);  // id rows first, then the window rows
   const T* kbase = reinterpret_cast<const T*>(s.k) + (size_t)h * s.hs;
   const T* vbase = reinterpret_cast<const T*>(s.v) + (size_t)h * s.hs;
   const T* wkb = reinterpret_cast<const T*>(s.wk) + (size_t)h * s.whs;

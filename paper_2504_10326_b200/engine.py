@@ -53,6 +53,24 @@ class SeqView:
     token_offset: int = 0
     prefix_len: int | None = None
     bounds: torch.Tensor | None = None  # [Hkv, blocks, 5, d] (block_bounds), block filter only
+    # CUDA-graph mode: int32 [1] device row count of the window ring (``w`` is ignored;
+    # the capacity is wk.shape[1]); window_append advances it on the device
+    w_dev: torch.Tensor | None = None
+
+
+def _w_dev_ptr(s: SeqView):
+    if s.w_dev is None:
+        return None
+    if s.w_dev.dtype != torch.int32 or not s.w_dev.is_cuda or s.w_dev.numel() < 1:
+        raise ValueError("w_dev must be an int32 CUDA tensor")
+    if s.wk is None or s.wv is None:
+        raise ValueError("w_dev needs the window ring tensors")
+    return s.w_dev.data_ptr()
+
+
+def _window_rows(s: SeqView) -> int:
+    """Host row count, or the ring capacity in device-count (graph) mode."""
+    return int(s.wk.shape[1]) if s.w_dev is not None and s.wk is not None else int(s.w)
 
 
 def _check_kv(t: torch.Tensor, name: str, dtype, d: int) -> None:
@@ -90,17 +108,19 @@ def seq_array(seqs: list[SeqView], params: AlayaParams, dtype: torch.dtype):
             if s.v.stride(0) != s.k.stride(0):
                 raise ValueError("k and v must share a head stride")
             e.k, e.v, e.head_stride = s.k.data_ptr(), s.v.data_ptr(), s.k.stride(0)
-        if s.w:
+        w = _window_rows(s)
+        if w:
             _check_kv(s.wk, "wk", dtype, d)
             _check_kv(s.wv, "wv", dtype, d)
-            if s.wk.shape[1] < s.w or s.wv.stride(0) != s.wk.stride(0):
+            if s.wk.shape[1] < w or s.wv.stride(0) != s.wk.stride(0):
                 raise ValueError("window K/V shape mismatch")
             e.wk, e.wv, e.w_head_stride = s.wk.data_ptr(), s.wv.data_ptr(), s.wk.stride(0)
         if s.bounds is not None:
             if s.bounds.dtype != dtype or not s.bounds.is_contiguous() or s.bounds.shape[0] != params.n_kv_heads:
                 raise ValueError("bounds must be a contiguous [Hkv, blocks, 5, d] tensor in the KV dtype")
             e.bounds, e.bounds_head_stride = s.bounds.data_ptr(), s.bounds.stride(0)
-        e.n, e.w = int(s.n), int(s.w)
+        e.n, e.w = int(s.n), w
+        e.d_w = _w_dev_ptr(s)
         e.token_offset = int(s.token_offset)
         e.prefix_len = int(s.n + s.token_offset if s.prefix_len is None else s.prefix_len)
     return arr
@@ -394,7 +414,8 @@ def append_array(seqs: list[SeqView], params: AlayaParams, dtype: torch.dtype):
         _check_kv(s.wv, "wv", dtype, params.dim)
         e = arr[i]
         e.wk, e.wv, e.w_head_stride = s.wk.data_ptr(), s.wv.data_ptr(), s.wk.stride(0)
-        e.w = int(s.w)
+        e.w = _window_rows(s)
+        e.d_w = _w_dev_ptr(s)
     return arr
 
 

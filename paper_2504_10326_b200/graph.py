@@ -1,0 +1,76 @@
+"""A whole decode step captured once as a CUDA graph (small-batch / short-context
+decode, where the per-call host path -- descriptor marshalling, ctypes, tensor-map
+encoding, a dozen launches per layer -- costs more than the GPU work).
+
+For every layer the step is ``Session.update`` (window append, reference
+``store.py:160-189``) followed by ``Session.attention`` on the DIPR/FLAT plan
+(``store.py:191-216``) over all sessions of the batch, i.e. exactly the calls
+``bench.py`` issues eagerly. The window row count lives on the device
+(``SeqView.w_dev`` -> ``alaya_seq.d_w``): the append kernel writes row ``*d_w`` and a
+commit kernel advances it, so one capture stays valid while the windows grow (up
+to the ring capacity). Inputs go through static buffers: write the step's
+``q``/``k``/``v`` into :attr:`q`, :attr:`k`, :attr:`v`, call :meth:`replay`, read
+:attr:`out`.
+
+Not for the fused sharded step (its exchange epochs are per call).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import engine
+
+
+class DecodeStepGraph:
+    """``layers``: per layer the ``SeqView`` list of the batch (all with ``w_dev``
+    set, one counter per (session, layer)) -- the append targets and the attention
+    inputs are the same views."""
+
+    def __init__(self, layers: list[list[engine.SeqView]], params, dtype: torch.dtype,
+                 device: torch.device):
+        if not layers or any(len(l) != len(layers[0]) for l in layers):
+            raise ValueError("every layer needs the same batch of sequences")
+        if any(s.w_dev is None for l in layers for s in l):
+            raise ValueError("graph mode needs SeqView.w_dev (device window counts)")
+        self.L, self.B = len(layers), len(layers[0])
+        hq, hkv, d = params.n_query_heads, params.n_kv_heads, params.dim
+        self.params, self.dtype, self.device = params, dtype, device
+        self.q = torch.zeros(self.L, self.B, hq, d, dtype=torch.float32, device=device)
+        self.k = torch.zeros(self.L, self.B, hkv, d, dtype=torch.float32, device=device)
+        self.v = torch.zeros_like(self.k)
+        self.out = torch.zeros_like(self.q)
+        # the graph owns its workspace (the layers run back to back, as eagerly): a shared
+        # buffer could be reallocated under the captured pointers
+        self.calls = [engine.Call(l, params, dtype, device) for l in layers]
+        self.ws = torch.empty(max(c.ws_bytes for c in self.calls), dtype=torch.uint8, device=device)
+        for c in self.calls:
+            c.ws, c.ws_bytes = self.ws, self.ws.numel()
+        self.appends = [engine.append_array(l, params, dtype) for l in layers]
+        self.counters = [s.w_dev for l in layers for s in l]
+        self.graph = torch.cuda.CUDAGraph()
+        self._capture()
+
+    def _step(self) -> None:
+        for l in range(self.L):
+            engine.window_append_raw(self.appends[l], self.B, self.params, self.k[l], self.v[l])
+            self.calls[l].dipr_attention(self.q[l], out=self.out[l])
+
+    def _capture(self) -> None:
+        saved = [c.clone() for c in self.counters]
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):  # one eager step first (lazy per-kernel setup), then undo it
+            self._step()
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        for c, v in zip(self.counters, saved):
+            c.copy_(v)
+        torch.cuda.synchronize(self.device)
+        with torch.cuda.graph(self.graph):
+            self._step()
+        torch.cuda.synchronize(self.device)
+
+    def replay(self) -> torch.Tensor:
+        """One decode step of every layer (stream-ordered); returns :attr:`out`."""
+        self.graph.replay()
+        return self.out
