@@ -41,23 +41,46 @@ __device__ __forceinline__ void hist_add(unsigned* hist, unsigned bin) {
 __device__ __forceinline__ void pick_bin(unsigned* hist, int shift, bool desc, uint64_t& prefix,
                                          uint64_t& mask, long long& kk, bool& found,
                                          unsigned* s_pop) {
+  // the bin holding the kk-th element in scan order (desc: 255..0): warp 0, each
+  // lane 8 consecutive bins, one warp prefix sum, the first lane whose inclusive
+  // sum reaches kk scans its own 8 bins (a serial 256-bin loop cost ~5 us a pass)
   __syncthreads();
-  if (threadIdx.x == 0) {
-    long long cum = 0;
-    found = false;
-    for (int i = 0; i < 256; ++i) {
-      const int bin = desc ? 255 - i : i;
-      const long long hbin = hist[bin];
-      if (cum + hbin >= kk) {
-        prefix |= (uint64_t)bin << shift;
-        kk -= cum;
-        found = true;
-        *s_pop = (unsigned)hbin;
-        break;
-      }
-      cum += hbin;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    unsigned v[8];
+    long long loc = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int i = lane * 8 + t;
+      v[t] = hist[desc ? 255 - i : i];
+      loc += v[t];
     }
-    mask |= (uint64_t)255 << shift;
+    long long inc = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const long long want = kk;
+    const unsigned hit = __ballot_sync(0xffffffffu, inc >= want);
+    if (hit == 0u) {
+      if (lane == 0) found = false;
+    } else if (lane == __ffs(hit) - 1) {
+      long long cum = inc - loc;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        if (cum + v[t] >= want) {
+          const int i = lane * 8 + t;
+          prefix |= (uint64_t)(desc ? 255 - i : i) << shift;
+          kk = want - cum;
+          found = true;
+          *s_pop = v[t];
+          break;
+        }
+        cum += v[t];
+      }
+    }
+    if (lane == 0) mask |= (uint64_t)255 << shift;
   }
   __syncthreads();
 }
@@ -155,55 +178,56 @@ template <typename T, int D>
 __global__ void __launch_bounds__(256)
     topk_sample_kernel(const __grid_constant__ Batch bt, const float* __restrict__ q,
                        float* __restrict__ samp, int S_max) {
-  constexpr int DL = (D + 31) / 32;
-  constexpr int RU = 8;
+  // one THREAD per sampled key, all G heads: the key row is read as 16-byte
+  // vectors (L1-cached), q comes from smem by broadcast, no shuffle reductions
+  // (a warp-per-key layout spent its time in 2 warp sums per key and head)
+  constexpr int V = 16 / (int)sizeof(T);  // elements per 16-byte load
+  __shared__ float s_q[kMaxG][D];
   pdl_trigger();
   pdl_wait();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.x / bt.Hkv, h = blockIdx.x - b * bt.Hkv;
   const KSeq& s = bt.s[b];
   const int G = bt.G;
   const int S = min(s.n, S_max);
-  float qr[kMaxG][DL];
+  for (int t = threadIdx.x; t < G * D; t += blockDim.x)
+    s_q[t / D][t % D] = __ldg(q + ((size_t)b * bt.Hq + h * G) * D + t);
+  __syncthreads();
+  const int i = blockIdx.y * blockDim.x + threadIdx.x;
+  if (i >= S) return;
+  const T* kr = reinterpret_cast<const T*>(s.k) + (size_t)h * s.hs + (size_t)((int64_t)i * s.n / S) * D;
+  float a[kMaxG], mag[kMaxG];
 #pragma unroll
-  for (int j = 0; j < kMaxG; ++j)
+  for (int j = 0; j < kMaxG; ++j) a[j] = mag[j] = 0.f;
 #pragma unroll
-    for (int k = 0; k < DL; ++k) {
-      const int e = lane + 32 * k;
-      qr[j][k] = (j < G && e < D) ? __ldg(q + ((size_t)b * bt.Hq + h * G + j) * D + e) : 0.f;
-    }
-  const T* kb = reinterpret_cast<const T*>(s.k) + (size_t)h * s.hs;
-  const int i_base = blockIdx.y * 256 + warp * 32;
-  for (int i0 = i_base; i0 < min(i_base + 32, S); i0 += RU) {
-    float x[RU][DL];
+  for (int e0 = 0; e0 < D; e0 += V) {
+    const uint4 raw = __ldg(reinterpret_cast<const uint4*>(kr + e0));
+    float x[V];
+    if constexpr (std::is_same_v<T, float>) {
+      x[0] = __uint_as_float(raw.x); x[1] = __uint_as_float(raw.y);
+      x[2] = __uint_as_float(raw.z); x[3] = __uint_as_float(raw.w);
+    } else {
+      const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
-    for (int u = 0; u < RU; ++u) {
-      const int i = i0 + u;
-      const T* kr = kb + (size_t)((int64_t)min(i, S - 1) * s.n / S) * D;
-#pragma unroll
-      for (int k = 0; k < DL; ++k) {
-        const int e = lane + 32 * k;
-        x[u][k] = e < D ? to_f(kr[e]) : 0.f;
+      for (int t = 0; t < 4; ++t) {
+        x[2 * t] = __uint_as_float(w[t] << 16);
+        x[2 * t + 1] = __uint_as_float(w[t] & 0xffff0000u);
       }
     }
 #pragma unroll
-    for (int u = 0; u < RU; ++u) {
-      const int i = i0 + u;
+    for (int j = 0; j < kMaxG; ++j) {
+      if (j >= G) break;
 #pragma unroll
-      for (int j = 0; j < kMaxG; ++j) {
-        if (j >= G) break;
-        float a = 0.f, mag = 0.f;
-#pragma unroll
-        for (int k = 0; k < DL; ++k) {
-          a = fmaf(qr[j][k], x[u][k], a);
-          mag = fmaf(fabsf(qr[j][k]), fabsf(x[u][k]), mag);
-        }
-        a = warp_sum(a);
-        mag = warp_sum(mag);
-        if (lane == 0 && i < S && i < i_base + 32)
-          samp[((size_t)b * bt.Hq + h * G + j) * S_max + i] = a - 1e-3f * (mag + 1.f);
+      for (int t = 0; t < V; ++t) {
+        const float qv = s_q[j][e0 + t];
+        a[j] = fmaf(qv, x[t], a[j]);
+        mag[j] = fmaf(fabsf(qv), fabsf(x[t]), mag[j]);
       }
     }
+  }
+#pragma unroll
+  for (int j = 0; j < kMaxG; ++j) {
+    if (j >= G) break;
+    samp[((size_t)b * bt.Hq + h * G + j) * S_max + i] = a[j] - 1e-3f * (mag[j] + 1.f);
   }
 }
 
@@ -226,7 +250,8 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0) thr[row] = -INFINITY;
     return;
   }
-  for (int i = threadIdx.x; i < S; i += blockDim.x) s_u[i] = enc_max(samp[(size_t)row * S_max + i]);
+#pragma unroll 8
+  for (int i = threadIdx.x; i < S; i += blockDim.x) s_u[i] = enc_max(__ldg(samp + (size_t)row * S_max + i));
   if (threadIdx.x == 0) { s_prefix = 0; s_mask = 0; s_kk = k; s_found = true; }
   for (int shift = 24; shift >= 0; shift -= 8) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
