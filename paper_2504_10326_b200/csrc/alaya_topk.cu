@@ -271,20 +271,26 @@ __global__ void __launch_bounds__(256)
 // chunk_topk_kernel may have pruned each pair to its local top-k). The row's
 // list offsets are prefix-summed in smem, so every pass is one flat parallel
 // loop; when the elements fit, they are staged in smem once (key, local id).
-constexpr int kStageMax = 16384;  // elements staged in smem (128 KB)
-
+// The row's candidate keys are staged in smem once (encoded scores only, up to
+// stage_cap, sized from the free smem at launch) by a segment walk: warp w copies
+// segments w, w+W, ... coalesced, so no element needs a search for its segment.
+// Local ids are read from global memory only where they are needed (ties at the
+// threshold, and the selected elements in the collect pass), again per segment.
 __global__ void __launch_bounds__(kSelThreads)
     topk_select_kernel(const __grid_constant__ Batch bt, Ws ws, int k, int64_t* __restrict__ ids,
-                       float* __restrict__ scores, int64_t cap, int32_t* __restrict__ count) {
-  extern __shared__ uint32_t s_dyn[];  // [nseg + 1] offsets, then [kStageMax] keys + [kStageMax] lids
+                       float* __restrict__ scores, int64_t cap, int32_t* __restrict__ count, int stage_cap) {
+  extern __shared__ uint32_t s_dyn[];  // [nseg + 1] offsets, then [stage_cap] encoded keys
   __shared__ unsigned hist[256];
   __shared__ uint64_t s_prefix, s_mask, s_idprefix, s_idmask;
   __shared__ long long s_kk;
   __shared__ bool s_found;
   __shared__ unsigned s_pop;
   __shared__ int s_n;
+  __shared__ int s_wsum[kSelThreads / 32];
   pdl_trigger();
   pdl_wait();
+  constexpr int NW = kSelThreads / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int row = blockIdx.x;
   const int b = row / bt.Hq, qh = row - b * bt.Hq, h = qh / bt.G, j = qh - h * bt.G;
   const KSeq& sq = bt.s[b];
@@ -292,45 +298,60 @@ __global__ void __launch_bounds__(kSelThreads)
   const int nseg = nch * 4;
   int* s_off = reinterpret_cast<int*>(s_dyn);
   uint32_t* s_key = s_dyn + nseg + 1;
-  int* s_lid = reinterpret_cast<int*>(s_key + kStageMax);
-  // segment g = (chunk cc = g / 4, sub-list q = g % 4): counts, then an exclusive scan
-  for (int g = threadIdx.x; g < nseg; g += blockDim.x)
-    s_off[g + 1] = ws.cnt[((size_t)(c0 + g / 4) * bt.G + j) * 4 + (g & 3)];
-  if (threadIdx.x == 0) s_off[0] = 0;
-  __syncthreads();
-  if (threadIdx.x == 0)
-    for (int g = 1; g <= nseg; ++g) s_off[g] += s_off[g - 1];
-  __syncthreads();
+  auto seg_base = [&](int g) {  // first workspace slot of segment g = (chunk g / 4, sub-list g % 4)
+    return ((size_t)(c0 + g / 4) * bt.G + j) * chunk + (size_t)(g & 3) * qcap;
+  };
+  // segment counts -> exclusive offsets (block scan: each thread a contiguous run)
+  {
+    const int per = (nseg + kSelThreads - 1) / kSelThreads;
+    const int g0 = min(nseg, threadIdx.x * per), g1 = min(nseg, g0 + per);
+    int loc = 0;
+    for (int g = g0; g < g1; ++g) loc += ws.cnt[((size_t)(c0 + g / 4) * bt.G + j) * 4 + (g & 3)];
+    int inc = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_wsum[warp] = inc;
+    __syncthreads();
+    int wpre = 0;
+    for (int w = 0; w < warp; ++w) wpre += s_wsum[w];
+    int run = wpre + inc - loc;
+    for (int g = g0; g < g1; ++g) {
+      s_off[g] = run;
+      run += ws.cnt[((size_t)(c0 + g / 4) * bt.G + j) * 4 + (g & 3)];
+    }
+    if (threadIdx.x == kSelThreads - 1) s_off[nseg] = wpre + inc;
+    __syncthreads();
+  }
   const int total = s_off[nseg];
-  // element e -> (score, local id = cc * chunk + position in the chunk)
+  // element e -> (score, local id = cc * chunk + position in the chunk) (unstaged rows)
   auto fetch = [&](int e, float& sc, int& lid) {
     int lo = 0, hi = nseg - 1;
     while (lo < hi) {  // last segment with s_off[g] <= e
       const int mid = (lo + hi + 1) >> 1;
       if (s_off[mid] <= e) lo = mid; else hi = mid - 1;
     }
-    const int cc = lo >> 2, q = lo & 3;
-    const size_t cj = (size_t)(c0 + cc) * bt.G + j;
-    const size_t at = cj * chunk + q * qcap + (e - s_off[lo]);
+    const size_t at = seg_base(lo) + (e - s_off[lo]);
     sc = ws.cscore[at];
-    lid = cc * chunk + ws.cidx[at];
+    lid = (lo >> 2) * chunk + ws.cidx[at];
   };
-  const bool staged = total <= kStageMax;
+  const bool staged = total <= stage_cap;
   if (staged) {
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {
-      float sc;
-      int lid;
-      fetch(e, sc, lid);
-      s_key[e] = enc_max(sc);
-      s_lid[e] = lid;
+    for (int g = warp; g < nseg; g += NW) {
+      const int o = s_off[g], len = s_off[g + 1] - o;
+      const float* src = ws.cscore + seg_base(g);
+      for (int t = lane; t < len; t += 32) s_key[o + t] = enc_max(src[t]);
     }
     __syncthreads();
   }
-  auto elem = [&](int e, uint32_t& u, int& lid) {
-    if (staged) { u = s_key[e]; lid = s_lid[e]; return; }
+  auto key = [&](int e) -> uint32_t {
+    if (staged) return s_key[e];
     float sc;
+    int lid;
     fetch(e, sc, lid);
-    u = enc_max(sc);
+    return enc_max(sc);
   };
   if (threadIdx.x == 0) { s_prefix = 0; s_mask = 0; s_kk = k; s_n = 0; s_found = true; }
   // 1) threshold key T: the k-th largest encoded score
@@ -339,9 +360,7 @@ __global__ void __launch_bounds__(kSelThreads)
     __syncthreads();
     const uint32_t pre = (uint32_t)s_prefix, msk = (uint32_t)s_mask;
     for (int e = threadIdx.x; e < total; e += blockDim.x) {
-      uint32_t u;
-      int lid;
-      elem(e, u, lid);
+      const uint32_t u = key(e);
       if ((u & msk) == pre) hist_add(hist, (u >> shift) & 255);
     }
     pick_bin(hist, shift, true, s_prefix, s_mask, s_kk, s_found, &s_pop);
@@ -351,6 +370,25 @@ __global__ void __launch_bounds__(kSelThreads)
   const uint32_t T = (uint32_t)s_prefix;
   const long long need = s_kk;          // elements equal to T to take
   const bool ties = !all && (long long)s_pop > need;
+  // visit every element as (encoded key, local-id loader): segment walk when staged
+  auto visit = [&](auto&& fn) {
+    if (staged) {
+      for (int g = warp; g < nseg; g += NW) {
+        const int o = s_off[g], len = s_off[g + 1] - o;
+        const size_t base = seg_base(g);
+        const int lid0 = (g >> 2) * chunk;
+        for (int t = lane; t < len; t += 32)
+          fn(s_key[o + t], [&] { return lid0 + ws.cidx[base + t]; });
+      }
+    } else {
+      for (int e = threadIdx.x; e < total; e += blockDim.x) {
+        float sc;
+        int lid;
+        fetch(e, sc, lid);
+        fn(enc_max(sc), [&] { return lid; });
+      }
+    }
+  };
   // 2) among the ties at T, the need-th smallest local id (= smallest token id)
   __syncthreads();
   if (threadIdx.x == 0) { s_idprefix = 0; s_idmask = 0; s_kk = need; }
@@ -360,29 +398,27 @@ __global__ void __launch_bounds__(kSelThreads)
       for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
       __syncthreads();
       const uint32_t pre = (uint32_t)s_idprefix, msk = (uint32_t)s_idmask;
-      for (int e = threadIdx.x; e < total; e += blockDim.x) {
-        uint32_t u;
-        int lid;
-        elem(e, u, lid);
-        if (u == T && ((uint32_t)lid & msk) == pre) hist_add(hist, ((uint32_t)lid >> shift) & 255);
-      }
+      visit([&](uint32_t u, auto&& lid_of) {
+        if (u != T) return;
+        const uint32_t lid = (uint32_t)lid_of();
+        if ((lid & msk) == pre) hist_add(hist, (lid >> shift) & 255);
+      });
       pick_bin(hist, shift, false, s_idprefix, s_idmask, s_kk, s_found, &s_pop);
     }
   }
   const uint32_t Tid = ties ? (uint32_t)s_idprefix : 0xffffffffu;
   // 3) collect (set semantics: order is not part of the contract)
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {
-    uint32_t u;
-    int lid;
-    elem(e, u, lid);
-    if (all || u > T || (u == T && (uint32_t)lid <= Tid)) {
+  visit([&](uint32_t u, auto&& lid_of) {
+    if (!(all || u >= T)) return;
+    const int lid = lid_of();
+    if (all || u > T || (uint32_t)lid <= Tid) {
       const int o = atomicAdd(&s_n, 1);
       if (o < cap) {
         ids[(size_t)row * cap + o] = sq.off + lid;
         if (scores) scores[(size_t)row * cap + o] = dec_max(u);
       }
     }
-  }
+  });
   __syncthreads();
   if (threadIdx.x == 0) count[row] = min((int64_t)s_n, cap);
 }
@@ -782,11 +818,15 @@ int launch_topk_select(const Batch& bt, const Ws& ws, int k, int64_t* ids, float
   }
   int max_nch = 0;
   for (int b = 0; b < bt.B; ++b) max_nch = std::max(max_nch, bt.s[b].nch);
-  const size_t smem = (size_t)(max_nch * 4 + 1) * 4 + (size_t)kStageMax * 8;
-  if (smem > 227 * 1024) return fail(ALAYA_ERR_UNSUPPORTED, "top-k over %d chunks per head", max_nch);
+  // offsets, then as many staged keys as the remaining dynamic smem holds
+  const size_t off_bytes = (size_t)(max_nch * 4 + 1) * 4;
+  const size_t smem_max = 220 * 1024;
+  if (off_bytes + 4096 > smem_max) return fail(ALAYA_ERR_UNSUPPORTED, "top-k over %d chunks per head", max_nch);
+  const int stage_cap = (int)((smem_max - off_bytes) / 4);
+  const size_t smem = off_bytes + (size_t)stage_cap * 4;
   cudaFuncSetAttribute(topk_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   return launch_pdl("topk_select_kernel", topk_select_kernel, (unsigned)(bt.B * bt.Hq), kSelThreads, smem,
-                    st, bt, ws, k, ids, scores, cap, count);
+                    st, bt, ws, k, ids, scores, cap, count, stage_cap);
 }
 
 int launch_sparse_attention(const Batch& bt, int dtype, const float* q, const int64_t* ids, int64_t cap,

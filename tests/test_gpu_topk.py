@@ -178,3 +178,18 @@ def test_topk_batch_mixed_plans(cuda_ok, rng):
     o1, _, _ = O.session_attention_flat(q[0], keys[0], vals[0], None, None, 5.0)
     o2, _, _ = O.session_attention_topk(q[1], keys[0], vals[0], None, None, 50)
     assert rel(out[0], o1) <= TOL and rel(out[1], o2) <= TOL
+
+
+def test_flat_topk_unstaged_rows(cuda_ok, rng):
+    """Rows with more candidates than the select kernel stages in smem (k above the
+    sample count: every token is a candidate) take the global-memory path."""
+    import paper_2504_10326_b200 as P
+    keys = rng.standard_normal((70000, 64)).astype(np.float32)
+    keys[:5000] = keys[5000:10000]  # exact ties straddle the cut
+    q = rng.standard_normal(64).astype(np.float32)
+    scores = O.inner_products(keys, q)
+    idx = P.FlatIndex(keys)
+    for k in (60000, 69999):
+        got = idx.top_k(q, k)
+        assert len(got) == k
+        assert topk_set_ok(got, O.flat_top_k(q, keys, k), scores, k), k
