@@ -103,6 +103,12 @@ typedef struct {
                           * sum_d max(q_d lo_d, q_d hi_d) is below LB - beta, LB
                           * = max score of the base-window tokens (a lower bound
                           * of the DIPR max). Exact: the DIPR set is unchanged. */
+  /* Optional DEVICE call sequence number (CUDA-graph mode): a u64 the captured step
+   * increments once per replay before its first layer. Inside a stream capture it
+   * gives every captured call a per-replay identity, so the scan can start on prep's
+   * published header (the eager fast path) in graphs too. NULL: calls captured in a
+   * graph wait for prep's completion instead. */
+  const unsigned long long* d_call_seq;
 } alaya_params;
 
 /* Coarse block index of one sequence's context (alaya_block_reps output):

@@ -69,6 +69,7 @@ class AlayaParams(ctypes.Structure):
         ("win_initial", ctypes.c_int32), ("win_last", ctypes.c_int32),
         ("chunk", ctypes.c_int32), ("scan_kind", ctypes.c_int32),
         ("block_filter", ctypes.c_int32),
+        ("d_call_seq", ctypes.c_void_p),
     ]
 
 

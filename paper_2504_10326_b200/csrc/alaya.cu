@@ -218,6 +218,7 @@ struct Call {
   Ws ws;
   StageSet st;
   cudaStream_t stream;
+  const unsigned long long* call_seq;  // params->d_call_seq
 };
 
 int prepare(const alaya_params* p, const alaya_seq* seqs, int B, void* d_ws, size_t ws_bytes,
@@ -237,6 +238,7 @@ int prepare(const alaya_params* p, const alaya_seq* seqs, int B, void* d_ws, siz
                 "16-byte aligned slabs with a head stride multiple of 128");
   c->use_tc = eligible && p->scan_kind != ALAYA_SCAN_CUDA_CORE;
   c->stream = static_cast<cudaStream_t>(stream);
+  c->call_seq = p->d_call_seq;
   return ALAYA_OK;
 }
 
@@ -252,10 +254,17 @@ int run_scan(Call& c, const float* d_q, bool ends_in_combine = true) {
   // (not inside a CUDA-graph capture: every replay would reuse the captured id)
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(c.stream, &cap) != cudaSuccess) cap = cudaStreamCaptureStatusActive;
-  c.bt.call_id = (async_prep && ends_in_combine && c.use_tc && !c.bt.block_filter && !c.bt.topk_thr &&
-                  cap == cudaStreamCaptureStatusNone)
-                     ? next_id++
-                     : 0ull;
+  const bool eligible = async_prep && ends_in_combine && c.use_tc && !c.bt.block_filter && !c.bt.topk_thr;
+  c.bt.call_seq = nullptr;
+  if (cap == cudaStreamCaptureStatusNone) {
+    c.bt.call_id = eligible ? next_id++ : 0ull;
+  } else if (eligible && c.call_seq) {  // graph: slot id (bit 63 + 20 bits) + the replay number
+    static std::atomic<unsigned long long> next_slot{0};
+    c.bt.call_id = (1ull << 63) | (next_slot++ & 0xFFFFFull);
+    c.bt.call_seq = c.call_seq;
+  } else {
+    c.bt.call_id = 0ull;
+  }
   int rc = c.st.prep(c.bt, d_q, c.ws, c.stream);  // zeroes the header, seeds the max
   if (rc) return rc;
   if (c.bt.block_filter) {

@@ -87,8 +87,9 @@ struct Batch {
   int32_t dbg;  // diagnostics only (ALAYA_TC_DBG): bit0 no L2 hint, bit1 no epilogue math, bit2 no MMA
   int32_t block_filter;
   int32_t split;  // attend task split threshold (candidates per (chunk, head) pair)
-  unsigned long long call_id;  // != 0: prep publishes the zeroed header as ws.ready = call_id and
+  unsigned long long call_id;  // != 0: prep publishes the zeroed header as ws.ready = call_token and
                                // seeds asynchronously (the tcgen05 scan waits on ready, not on prep)
+  const unsigned long long* call_seq;  // graph mode: per-replay sequence number (see call_token)
   int32_t seed;   // prep_kernel seeds the running max from sampled keys
   int32_t overlap;  // scan publishes per-group completion; attend runs beside it (PDL)
   const float* topk_thr;  // TOP_K: per-row candidate threshold (a lower bound of the k-th
@@ -103,6 +104,13 @@ struct BixSet {
 };
 
 // Workspace pointers (device), carved from the caller's buffer.
+// Identity of this call for the async-prep handshake: the host id, or in graph mode
+// (call_seq) the captured slot combined with the replay's sequence number, which the
+// graph's first node advances, so ids never repeat across replays.
+__device__ __forceinline__ unsigned long long call_token(const Batch& bt) {
+  return bt.call_seq ? (bt.call_id | (__ldcg(bt.call_seq) << 20)) : bt.call_id;
+}
+
 struct Ws {
   int* status;
   unsigned long long* ready;  // call id whose header prep has zeroed (next to status, never zeroed)

@@ -788,7 +788,7 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
       __threadfence();
       __syncthreads();
       if (threadIdx.x == 0)
-        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ws.ready), "l"(bt.call_id) : "memory");
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ws.ready), "l"(call_token(bt)) : "memory");
     }
   } else {
     if (blockIdx.x == 0 && threadIdx.x < 16) {
@@ -876,7 +876,8 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
       // bounded: a seed is optional (a lower bound), so a CTA that cannot see the
       // header published (CTA 0 not resident) drops its seed instead of spinning on
       int polls = 0;
-      while (ld_acquire_gpu_u64(ws.ready) != bt.call_id && ++polls < (1 << 20)) __nanosleep(32);
+      const unsigned long long tok = call_token(bt);
+      while (ld_acquire_gpu_u64(ws.ready) != tok && ++polls < (1 << 20)) __nanosleep(32);
       s_ok = polls < (1 << 20);
     }
     __syncthreads();
@@ -888,7 +889,8 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ws.seeded + blockIdx.x), "l"(bt.call_id) : "memory");
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ws.seeded + blockIdx.x), "l"(call_token(bt))
+                   : "memory");
       asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(&ws.counters[8]), "r"(1) : "memory");
     }
     return;

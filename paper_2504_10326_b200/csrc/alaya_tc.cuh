@@ -313,8 +313,10 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 4 : (kStages <= 3 
   // tickets), then triggers: a dependent launched after the trigger sees all
   // earlier work complete.
   if (warp != 0 && bt.call_id) {  // async prep: the zeroed header is published as ws.ready
-    if (lane == 0)
-      while (ld_acquire_gpu_u64(ws.ready) != bt.call_id) __nanosleep(32);
+    if (lane == 0) {
+      const unsigned long long tok = call_token(bt);
+      while (ld_acquire_gpu_u64(ws.ready) != tok) __nanosleep(32);
+    }
     __syncwarp();
   } else if (warp != 0 || bt.block_filter) {
     pdl_wait();
@@ -423,7 +425,8 @@ __global__ void __launch_bounds__(kThreadsTc, (kStages <= 2 ? 4 : (kStages <= 3 
         decode_chunk(bt, blockIdx.x, b, h, ci);
         if (lane == 0) {
           int polls = 0;
-          while (ld_acquire_gpu_u64(ws.seeded + b * bt.Hkv + h) != bt.call_id && ++polls < (1 << 20))
+          const unsigned long long tok = call_token(bt);
+          while (ld_acquire_gpu_u64(ws.seeded + b * bt.Hkv + h) != tok && ++polls < (1 << 20))
             __nanosleep(32);
         }
         __syncwarp();

@@ -13,6 +13,11 @@ to the ring capacity). Inputs go through static buffers: write the step's
 :attr:`out`.
 
 Not for the fused sharded step (its exchange epochs are per call).
+
+Graph-mode handshake: the step's first node advances a device sequence number
+(``alaya_params.d_call_seq``); each captured call combines it with its capture
+slot, so prep's published header is told apart from the previous replay's and the
+scan can start before prep finishes, as in the eager path.
 """
 
 from __future__ import annotations
@@ -35,6 +40,11 @@ class DecodeStepGraph:
             raise ValueError("graph mode needs SeqView.w_dev (device window counts)")
         self.L, self.B = len(layers), len(layers[0])
         hq, hkv, d = params.n_query_heads, params.n_kv_heads, params.dim
+        # replay sequence number (first node of the step): gives every captured call a
+        # per-replay identity, so the scan starts on prep's published header as eagerly
+        self.seq = torch.zeros(1, dtype=torch.int64, device=device)
+        params = type(params).from_buffer_copy(params)
+        params.d_call_seq = self.seq.data_ptr()
         self.params, self.dtype, self.device = params, dtype, device
         self.q = torch.zeros(self.L, self.B, hq, d, dtype=torch.float32, device=device)
         self.k = torch.zeros(self.L, self.B, hkv, d, dtype=torch.float32, device=device)
@@ -52,6 +62,7 @@ class DecodeStepGraph:
         self._capture()
 
     def _step(self) -> None:
+        self.seq.add_(1)
         for l in range(self.L):
             engine.window_append_raw(self.appends[l], self.B, self.params, self.k[l], self.v[l])
             self.calls[l].dipr_attention(self.q[l], out=self.out[l])
