@@ -193,3 +193,27 @@ def test_flat_topk_unstaged_rows(cuda_ok, rng):
         got = idx.top_k(q, k)
         assert len(got) == k
         assert topk_set_ok(got, O.flat_top_k(q, keys, k), scores, k), k
+
+
+def test_alternating_plans_share_the_workspace(cuda_ok, rng):
+    """DIPR calls (asynchronous prep handshake on the shared workspace) interleaved
+    with TOP_K calls (synchronous prep) and the CUDA-core scan stay exact call after
+    call: a stale header or seed from the previous call would show up here."""
+    import paper_2504_10326_b200 as P
+    L, hq, hkv, d, n = 1, 8, 2, 128, 6000
+    tok, keys, vals, centers, _ = O.make_context(n, L, hkv, d, seed=77)
+    keys, vals = O.bf16_round(keys), O.bf16_round(vals)
+    cfg = P.EngineConfig(short_context_threshold=0, first_layers=(0,), beta=5.0, top_k=64,
+                         kv_dtype="bfloat16")
+    db = P.ContextStore(P.ModelShape(L, hq, hkv, d), cfg)
+    db.import_context(tok, keys, vals)
+    s1, _ = db.create_session(tok)
+    s2, _ = db.create_session(tok)
+    s2.plan_override = P.Plan(P.QueryKind.TOP_K, P.IndexKind.FLAT, k=64)
+    for it in range(6):
+        q = (centers[rng.integers(0, 16, (2, hq))] + 0.25 * rng.standard_normal((2, hq, d))).astype(np.float32)
+        out = P.Session.attention_batch([s1, s2], q, 0) if it % 2 == 0 else np.stack(
+            [s1.attention(q[0], 0), s2.attention(q[1], 0)])
+        o1, _, _ = O.session_attention_flat(q[0], keys[0], vals[0], None, None, 5.0)
+        o2, _, _ = O.session_attention_topk(q[1], keys[0], vals[0], None, None, 64)
+        assert rel(out[0], o1) <= 2e-2 and rel(out[1], o2) <= 2e-2, it
