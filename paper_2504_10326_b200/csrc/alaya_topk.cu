@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(kSelThreads)
   const int nb = bi.n_blocks, r = bi.r;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int hl = lane & 15, hw = threadIdx.x >> 4;  // half-warp per representative row
-  constexpr int DPL = D / 16, U = 8, NHW = kSelThreads / 16;
+  constexpr int DPL = D / 16, U = 16, NHW = kSelThreads / 16;
   float qr[DPL];
   load_q<DPL>(q + (size_t)row * D + hl * DPL, qr);
   for (int i = threadIdx.x; i < nb; i += blockDim.x) s_score[i] = 0u;  // -inf
