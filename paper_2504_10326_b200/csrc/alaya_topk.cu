@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(kSelThreads)
 // Partial attention over explicit base ids (minus the window ids) merged with
 // the window partial; one CTA per (sequence, q head), warps take interleaved
 // row batches with their own online softmax, merged in fixed warp order.
-constexpr int kSaU = 4;        // rows in flight per half-warp
+constexpr int kSaU = 8;        // rows in flight per half-warp
 constexpr int kSaWarps = 16;   // warps per (sequence, q head)
 
 template <typename T, int D>
