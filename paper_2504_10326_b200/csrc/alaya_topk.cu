@@ -232,7 +232,8 @@ __global__ void __launch_bounds__(256)
 }
 
 // Per row: the k-th largest of its S samples -> thr[row] (-inf when S < k).
-__global__ void __launch_bounds__(256)
+constexpr int kThrThreads = 1024;
+__global__ void __launch_bounds__(kThrThreads)
     topk_thr_kernel(const __grid_constant__ Batch bt, const float* __restrict__ samp, int S_max, int k,
                     float* __restrict__ thr) {
   extern __shared__ uint32_t s_u[];  // [S_max]
@@ -803,7 +804,7 @@ int launch_topk_bound(const Batch& bt, int dtype, const float* q, float* scratch
   if (rc) return rc;
   const size_t smem = (size_t)S_max * 4;
   cudaFuncSetAttribute(topk_thr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  return launch_pdl("topk_thr_kernel", topk_thr_kernel, (unsigned)(bt.B * bt.Hq), 256, smem, st, bt, scratch,
+  return launch_pdl("topk_thr_kernel", topk_thr_kernel, (unsigned)(bt.B * bt.Hq), kThrThreads, smem, st, bt, scratch,
                     S_max, k, thr);
 }
 
