@@ -24,6 +24,7 @@ namespace alaya {
 namespace {
 
 constexpr int kSelThreads = 512;
+constexpr int kSelectThreads = 1024;  // topk_select_kernel
 
 // Histogram increment aggregated over the warp's active lanes that hit the same
 // bin: radix digits of nearby scores collide heavily, and per-lane shared atomics
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(kThrThreads)
 // segments w, w+W, ... coalesced, so no element needs a search for its segment.
 // Local ids are read from global memory only where they are needed (ties at the
 // threshold, and the selected elements in the collect pass), again per segment.
-__global__ void __launch_bounds__(kSelThreads)
+__global__ void __launch_bounds__(kSelectThreads)
     topk_select_kernel(const __grid_constant__ Batch bt, Ws ws, int k, int64_t* __restrict__ ids,
                        float* __restrict__ scores, int64_t cap, int32_t* __restrict__ count, int stage_cap) {
   extern __shared__ uint32_t s_dyn[];  // [nseg + 1] offsets, then [stage_cap] encoded keys
@@ -287,10 +288,10 @@ __global__ void __launch_bounds__(kSelThreads)
   __shared__ bool s_found;
   __shared__ unsigned s_pop;
   __shared__ int s_n;
-  __shared__ int s_wsum[kSelThreads / 32];
+  __shared__ int s_wsum[kSelectThreads / 32];
   pdl_trigger();
   pdl_wait();
-  constexpr int NW = kSelThreads / 32;
+  constexpr int NW = kSelectThreads / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int row = blockIdx.x;
   const int b = row / bt.Hq, qh = row - b * bt.Hq, h = qh / bt.G, j = qh - h * bt.G;
@@ -304,7 +305,7 @@ __global__ void __launch_bounds__(kSelThreads)
   };
   // segment counts -> exclusive offsets (block scan: each thread a contiguous run)
   {
-    const int per = (nseg + kSelThreads - 1) / kSelThreads;
+    const int per = (nseg + kSelectThreads - 1) / kSelectThreads;
     const int g0 = min(nseg, threadIdx.x * per), g1 = min(nseg, g0 + per);
     int loc = 0;
     for (int g = g0; g < g1; ++g) loc += ws.cnt[((size_t)(c0 + g / 4) * bt.G + j) * 4 + (g & 3)];
@@ -323,7 +324,7 @@ __global__ void __launch_bounds__(kSelThreads)
       s_off[g] = run;
       run += ws.cnt[((size_t)(c0 + g / 4) * bt.G + j) * 4 + (g & 3)];
     }
-    if (threadIdx.x == kSelThreads - 1) s_off[nseg] = wpre + inc;
+    if (threadIdx.x == kSelectThreads - 1) s_off[nseg] = wpre + inc;
     __syncthreads();
   }
   const int total = s_off[nseg];
@@ -826,7 +827,7 @@ int launch_topk_select(const Batch& bt, const Ws& ws, int k, int64_t* ids, float
   const int stage_cap = (int)((smem_max - off_bytes) / 4);
   const size_t smem = off_bytes + (size_t)stage_cap * 4;
   cudaFuncSetAttribute(topk_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  return launch_pdl("topk_select_kernel", topk_select_kernel, (unsigned)(bt.B * bt.Hq), kSelThreads, smem,
+  return launch_pdl("topk_select_kernel", topk_select_kernel, (unsigned)(bt.B * bt.Hq), kSelectThreads, smem,
                     st, bt, ws, k, ids, scores, cap, count, stage_cap);
 }
 
