@@ -492,8 +492,10 @@ int alaya_topk(const alaya_params* p, const alaya_seq* seqs, int batch, const fl
   for (int b = 0; b < batch; ++b)
     if (seqs[b].token_offset != 0 || seqs[b].prefix_len != seqs[b].n)
       return fail(ALAYA_ERR_UNSUPPORTED, "top-k runs on unsharded sequences");
-  // prep; the per-row candidate bound from sampled keys (scratch: the candidate
-  // score buffer, consumed before the scan writes it); the scan keeps s >= bound
+  // prep (header only: the DIPR seed is unused at beta = inf, the bound below replaces
+  // it); the per-row candidate bound from sampled keys (scratch: the candidate score
+  // buffer, consumed before the scan writes it); the scan keeps s >= bound
+  c.bt.seed = 0;
   if ((rc = c.st.prep(c.bt, d_q, c.ws, c.stream))) return rc;
   const size_t scratch = (size_t)(c.L.cscore_end - c.L.cscore) / 4;
   if ((rc = launch_topk_bound(c.bt, p->dtype, d_q, c.ws.cscore, scratch, k, c.ws.smaxbuf, c.stream))) return rc;
