@@ -9,9 +9,16 @@ B * L * Hq / step time (BASELINE.json).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-N > 1 (torchrun): sequence-sharded mode, weak scaling: B*N sessions, each
-rank holds 128K/N tokens of every session; NCCL max-allreduce of the DIPR
-threshold + allgather of the partial (m, l, acc) states per layer.
+N > 1 (torchrun): sequence-sharded mode. Each rank holds ctx/N tokens of every
+session; per layer the global DIPR max is a max-allreduce and the partial
+(m, l, acc) states are all-gathered and merged (over NVLink peer memory, fused
+into the kernels, or NCCL). ``--scaling weak`` runs batch*N sessions (per-rank
+bytes constant); ``--scaling strong`` runs batch sessions (total work constant),
+the default for ctx >= 1M (BASELINE config 5: one 1M-token context on 1..8 GPUs).
+The JSON line names the data plane that ran (``config.collectives``).
+
+--impl reference: the reference's own CPU path (the installed, unmodified
+sparsekv from baseline/_ref, else the pinned oracle port) on all host cores.
 """
 
 from __future__ import annotations
@@ -54,15 +61,38 @@ def parse():
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: warmup + steps only, no side measurements")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--scaling", default="auto", choices=["auto", "weak", "strong"],
+                    help="N>1: weak = batch*N sessions, each rank ctx/N of every one (per-rank "
+                         "bytes constant); strong = batch sessions, each rank ctx/N of them "
+                         "(total work constant). auto: strong for ctx >= 1M (config 5), else weak")
+    ap.add_argument("--diagnostics-e2e", action="store_true",
+                    help="also time the e2e path with EngineConfig.diagnostics on (selected ids "
+                         "exported every call, the reference's last_diagnostics)")
+    ap.add_argument("--cpu-variants", default="threads_1,threads_all,process_pool",
+                    help="cpu_baseline variants (tools/cpu_reference.py)")
     ap.add_argument("--check", action="store_true",
                     help="N>1: generate identical full contexts on every rank (small sizes) and "
                          "compare the sharded layer-0 output with the unsharded kernels")
     return ap.parse_args()
 
 
+def scaling_mode(a, world):
+    if world == 1:
+        return "weak"
+    if a.scaling == "auto":
+        return "strong" if a.ctx >= (1 << 20) else "weak"
+    return a.scaling
+
+
+def sessions_total(a, world):
+    return a.batch * world if scaling_mode(a, world) == "weak" else a.batch
+
+
 def workload_name(a, world):
-    return (f"llama3.1-8b-shape L{a.layers} Hq{a.hq}/Hkv{a.hkv} d{a.dim} ctx{a.ctx} "
-            f"B{a.batch * world} {'bf16' if a.kv_dtype == 'bfloat16' else 'fp32'} KV, "
+    shape = "llama3.1-8b-shape" if (a.hq, a.hkv) == (32, 8) else (
+        "qwen2.5-14b-shape" if (a.hq, a.hkv) == (40, 8) else "custom-shape")
+    return (f"{shape} L{a.layers} Hq{a.hq}/Hkv{a.hkv} d{a.dim} ctx{a.ctx} "
+            f"B{sessions_total(a, world)} {'bf16' if a.kv_dtype == 'bfloat16' else 'fp32'} KV, "
             f"flat DIPR beta={a.beta:g} + window 16+64")
 
 
@@ -167,18 +197,57 @@ def load_traffic(name):
 
 
 # ---------------------------------------------------------------------------
-# CPU reference (the oracle restatement of sparsekv, pinned bit-exact)
+# CPU reference: the installed reference (baseline/_ref) or the oracle port
 # ---------------------------------------------------------------------------
 
-def cpu_reference_time(keys, values, wk, wv, q, beta, reps=1):
-    """Seconds per Session.attention-equivalent call (all q heads) on the host."""
-    from oracle import alaya_oracle as O
-    ts = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        O.session_attention_flat(q, keys, values, wk, wv, beta)
-        ts.append(time.perf_counter() - t0)
-    return min(ts)
+def run_reference(a):
+    """--impl reference: the reference's own CPU path (unmodified sparsekv
+    Session.attention on the flat DIPR plan when baseline/_ref is installed,
+    else the pinned oracle port) on all host cores, on this arm's metric."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from tools.cpu_reference import CpuWorkload, cpu_info, variants
+    wl = CpuWorkload(a.ctx, a.hq, a.hkv, a.dim, a.beta, a.kv_dtype == "bfloat16",
+                     max(1, a.window_rows), max(1, a.steps + a.warmup), seed=a.seed)
+    v = variants(wl, a.steps, a.warmup, ("process_pool",))["process_pool"]
+    value, t, cores = v["value"], v["seconds_per_call"], v["cores"]
+    sample = (f"1 session x 1 layer per step ({a.hq} q heads, ctx {a.ctx}, "
+              f"{a.kv_dtype} KV widened to fp32), {wl.kind} generator seed {a.seed}; "
+              f"{'sparsekv Session._head_attention (store.py:252-293)' if wl.kind == 'reference' else 'oracle port'}"
+              f" per q head over a fork pool of {cores} processes on {cpu_info()}")
+    line = {"metric": METRIC, "value": value, "unit": "queries*heads/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": scaling_mode(a, world), "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (reference generator)",
+            "config": {"workload": workload_name(a, world) + " [CPU: one session-layer per step]"},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "queries*heads/s", "cores": cores,
+                             "kind": wl.kind, "sample": sample},
+            "e2e": {"value": value, "unit": "queries*heads/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_leg(a):
+    """cpu_baseline of the GPU arm: bounded sample (one session-layer per call,
+    2 timed calls per variant) of the same workload on this host."""
+    from tools.cpu_reference import CpuWorkload, cpu_info, variants
+    wl = CpuWorkload(a.ctx, a.hq, a.hkv, a.dim, a.beta, a.kv_dtype == "bfloat16",
+                     max(1, a.window_rows), 4, seed=a.seed)
+    which = tuple(x for x in a.cpu_variants.split(",") if x)
+    vs = variants(wl, 2, 1, which)
+    best = max(vs, key=lambda k: vs[k]["value"])
+    return {"value": vs[best]["value"], "unit": "queries*heads/s", "cores": vs[best]["cores"],
+            "kind": wl.kind, "variant": best,
+            "sample": (f"1 session x 1 layer ({a.hq} q heads) at ctx {a.ctx}, "
+                       f"{'unmodified sparsekv Session.attention / _head_attention' if wl.kind == 'reference' else 'oracle port'}"
+                       f", reference generator seed {a.seed}, 2 timed calls per variant; "
+                       f"host {cpu_info()}, {os.cpu_count()} cores"),
+            "variants": {k: {"value": round(x["value"], 2), "cores": x["cores"],
+                             "seconds_per_call": round(x["seconds_per_call"], 3)}
+                         for k, x in vs.items()}}
 
 
 def blas_threads():
@@ -187,47 +256,6 @@ def blas_threads():
         return max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
     except Exception:
         return os.cpu_count() or 1
-
-
-def run_reference(a):
-    """--impl reference: the reference algorithm (oracle port) on host cores."""
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    if rank != 0:
-        return
-    import numpy as np
-    from oracle import alaya_oracle as O
-    tok, keys, vals, centers, _ = O.make_context(a.ctx, 1, a.hkv, a.dim, seed=a.seed)
-    if a.kv_dtype == "bfloat16":
-        keys, vals = O.bf16_round(keys), O.bf16_round(vals)
-    _, q, k, v = O.decode_step_inputs(a.steps + a.warmup, 1, a.hq, a.hkv, a.dim, centers,
-                                      seed=a.seed)
-    wrows = max(1, a.window_rows)
-    r = np.random.default_rng(a.seed + 5)
-    wk = O.bf16_round(r.standard_normal((a.hkv, wrows, a.dim)).astype(np.float32))
-    wv = O.bf16_round(r.standard_normal((a.hkv, wrows, a.dim)).astype(np.float32))
-    times = []
-    for s in range(a.warmup + a.steps):
-        t0 = time.perf_counter()
-        O.session_attention_flat(q[s, 0], keys[0], vals[0], wk, wv, a.beta)
-        if s >= a.warmup:
-            times.append(time.perf_counter() - t0)
-    t = statistics.mean(times)
-    value = a.hq / t
-    sample = (f"1 session x 1 layer per step ({a.hq} q heads, ctx {a.ctx}, Llama shape, "
-              f"{a.kv_dtype} KV widened to fp32), reference generator seed {a.seed}")
-    cores = blas_threads()
-    line = {"metric": METRIC, "value": value, "unit": "queries*heads/s", "n_gpus": world,
-            "steps": a.steps, "warmup": a.warmup, "ms_per_step": t * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (reference generator)",
-            "config": {"workload": workload_name(a, 1) + " [CPU: one session-layer per step]"},
-            "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": "queries*heads/s", "cores": cores,
-                             "kind": "port", "sample": sample},
-            "e2e": {"value": value, "unit": "queries*heads/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------
@@ -264,7 +292,8 @@ def main():
     dtype = torch.bfloat16 if a.kv_dtype == "bfloat16" else torch.float32
     esize = 2 if dtype == torch.bfloat16 else 4
     L, Hq, Hkv, d = a.layers, a.hq, a.hkv, a.dim
-    B = a.batch * world                      # sessions (global batch)
+    mode = scaling_mode(a, world)
+    B = sessions_total(a, world)             # sessions (global batch)
     if a.ctx % world:
         raise SystemExit("ctx must divide by the number of GPUs")
     n_loc = a.ctx // world                   # tokens of every session held by this rank
@@ -319,7 +348,9 @@ def main():
     stages = [EngineStages.from_call(c) for c in calls]
     # sharded collectives over peer memory (NVLink P2P via CUDA IPC, alaya_exch) unless
     # ALAYA_P2P=0; validated against the NCCL path on a real layer before use, NCCL otherwise
-    exch, collective = None, "none" if world == 1 else "nccl"
+    # the data plane that actually runs: NCCL over NVLink, gloo (shared-GPU validation
+    # only, staged through host memory), or our peer-memory kernels (p2p / p2p-fused)
+    exch, collective = None, "none" if world == 1 else ("gloo" if share else "nccl")
     if world > 1 and os.environ.get("ALAYA_P2P", "1") != "0":
         exch = PeerExchange.create(None, B * Hq * (d + 2), dev)
         ok = exch is not None
@@ -469,21 +500,20 @@ def main():
             errs.append(float(np.linalg.norm(o_gpu[qh] - ref) / np.linalg.norm(ref)))
         parity = {"heads_checked": len(errs), "max_norm_rel_err": max(errs),
                   "tolerance": 2e-2 if dtype == torch.bfloat16 else 1e-5}
-        t_cpu = cpu_reference_time(kh, vh, wkh, wvh, qh_, a.beta, reps=1)
-        cpu = {"value": Hq / t_cpu, "unit": "queries*heads/s", "cores": blas_threads(),
-               "kind": "port",
-               "sample": f"1 session x 1 layer ({Hq} q heads) at ctx {a.ctx}, oracle restatement "
-                         f"of sparsekv Session.attention (fp64), {t_cpu:.2f} s"}
+        cpu = cpu_baseline_leg(a)
 
     # --- e2e through the public Session API with host buffers
     e2e = None
     if not a.no_e2e and world == 1:
         e2e = run_e2e(a, P, torch, K, V, centers, dev, dtype)
+        if a.diagnostics_e2e:
+            e2e["with_diagnostics"] = run_e2e(a, P, torch, K, V, centers, dev, dtype,
+                                              diagnostics=True)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "queries*heads/s", "n_gpus": world,
                 "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "higher_is_better": True, "scaling": mode, "vs_baseline": None,
                 "dtype": "bf16" if dtype == torch.bfloat16 else "f32",
                 "data": "synthetic (reference generator distribution, drawn on GPU)",
                 "config": {"workload": name, "layers": L, "batch": B, "ctx": a.ctx,
@@ -511,7 +541,7 @@ def main():
         dist.destroy_process_group()
 
 
-def run_e2e(a, P, torch, K, V, centers, dev, dtype):
+def run_e2e(a, P, torch, K, V, centers, dev, dtype, diagnostics=False):
     """Same metric through the public API (Session.update_batch +
     Session.attention_batch per layer): every step copies that step's q/k/v
     from pinned host memory and reads all layer outputs back to pinned host."""
@@ -519,7 +549,7 @@ def run_e2e(a, P, torch, K, V, centers, dev, dtype):
     L, B, Hq, Hkv, d = a.layers, a.batch, a.hq, a.hkv, a.dim
     shape = P.ModelShape(L, Hq, Hkv, d)
     cfg = P.EngineConfig(beta=a.beta, first_layers=tuple(range(L)), short_context_threshold=0,
-                         kv_dtype=a.kv_dtype, scan_kernel=a.scan_kernel, diagnostics=False)
+                         kv_dtype=a.kv_dtype, scan_kernel=a.scan_kernel, diagnostics=diagnostics)
     db = P.ContextStore(shape, cfg, device=dev, log_queries=False)
     sessions = []
     for b in range(B):

@@ -41,6 +41,16 @@ def inner_products(keys: np.ndarray, q: np.ndarray) -> np.ndarray:
     return keys.astype(np.float64, copy=False) @ q.astype(np.float64, copy=False)
 
 
+def group_scores(keys: np.ndarray, qs: np.ndarray) -> np.ndarray:
+    """fp64 scores of a GQA group's query heads over one kv head's keys,
+    ``(n, G)`` = ``inner_products(keys, qs[j])`` for every j in one GEMM
+    (``core.py:64-67`` per head; the group shares ``kv_head_of``, ``core.py:108-112``)."""
+    qs = np.atleast_2d(qs)
+    if keys.shape[-1] != qs.shape[-1]:
+        raise ValueError(f"dimension mismatch: {keys.shape[-1]} vs {qs.shape[-1]}")
+    return keys.astype(np.float64, copy=False) @ qs.astype(np.float64, copy=False).T
+
+
 def scaled_scores(keys: np.ndarray, q: np.ndarray) -> np.ndarray:
     """Raw scores divided by sqrt(d) -- reference ``core.py:75-77``."""
     return inner_products(keys, q) / np.sqrt(q.shape[-1])
@@ -184,6 +194,18 @@ def head_attention_flat(q, base_k, base_v, win_k, win_v, beta, initial=16, last=
         selected = np.asarray(selected_override, dtype=np.int64)
     else:
         selected = np.setdiff1d(retrieved, window_ids)  # store.py:271-273
+    o = head_attention_on_selection(q, base_k, base_v, win_k, win_v, selected, initial, last)
+    return o, np.sort(selected), int(retrieved.size)
+
+
+def head_attention_on_selection(q, base_k, base_v, win_k, win_v, selected, initial=16, last=64):
+    """The tail of ``_head_attention`` for a given selection (``store.py:274-293``):
+    partial over the selected base rows, merged with the partial over the base
+    window rows + session window rows, finalized. Used on its own when the
+    caller already holds the fp64 scores (large parity cases)."""
+    p = base_k.shape[0]
+    window_ids = window_base_ids(p, initial, last)
+    selected = np.asarray(selected, dtype=np.int64)
     part = Partial()
     if selected.size:  # store.py:274-278
         part = partial_merge(part, partial_over(q, base_k[selected], base_v[selected]))
@@ -195,7 +217,7 @@ def head_attention_flat(q, base_k, base_v, win_k, win_v, beta, initial=16, last=
     if win_keys:
         part = partial_merge(
             part, partial_over(q, np.concatenate(win_keys), np.concatenate(win_vals)))
-    return partial_finalize(part), np.sort(selected), int(retrieved.size)
+    return partial_finalize(part)
 
 
 def session_attention_flat(q, base_k, base_v, win_k=None, win_v=None, beta=110.0,

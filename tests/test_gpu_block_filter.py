@@ -9,6 +9,7 @@ import pytest
 import torch
 
 from oracle import alaya_oracle as O
+from tests.parity import EPS_SET, set_flips
 
 pytestmark = pytest.mark.gpu
 
@@ -81,9 +82,13 @@ def test_filter_is_exact_and_prunes_with_locality(cuda_ok, kv, scan, beta):
     # same rows, but pruned tiles change candidate batching -> summation order
     assert rel(outs[1], outs[0].astype(np.float64)) <= 1e-6
     ref, rsel, _ = O.session_attention_flat(q, keys[0], vals[0], None, None, beta)
+    window = O.window_base_ids(n)
     for qh in range(hkv * g):
-        flips = set(sels[1][qh]) ^ set(rsel[qh].tolist())
-        assert len(flips) <= 1
+        h = qh // g
+        flips, _ = set_flips(sels[1][qh], O.inner_products(keys[0, h], q[qh]), beta,
+                             EPS_SET[kv], window)
+        o_sel = O.head_attention_on_selection(q[qh], keys[0, h], vals[0, h], None, None, sels[1][qh])
+        assert rel(outs[1][qh], o_sel) <= 1e-5
         if not flips:
             assert rel(outs[1][qh], ref[qh]) <= 1e-5
 
