@@ -362,7 +362,7 @@ int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch
     if (seqs[b].prefix_len + seqs[b].w == 0) return fail(ALAYA_ERR_ARG, "attention on an empty session");
   // attend beside the scan (per-group readiness); the CUDA-core scan fills the
   // register file (no room for an attend CTA: measured no gain), so tcgen05 only
-  if (c.use_tc && overlap_enabled(c.bt.B * c.bt.Hkv)) {
+  if (c.use_tc && overlap_enabled()) {
     c.bt.overlap = 1;
     if ((rc = run_scan(c, d_q))) return rc;
     if ((rc = c.st.attend_ovl(c.bt, d_q, c.ws, c.stream))) return rc;

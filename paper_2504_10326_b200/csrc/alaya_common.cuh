@@ -118,7 +118,7 @@ struct Ws {
   uint32_t* gmax;   // [B*Hq] order-preserving encoded running max
   int* counters;    // [16] right after gmax (zeroed by prep_kernel): [0] attend ticket,
                     // [2..3] block-filter kept/total, [6] epilogue-warp chunk publications
-                    // (overlapped attend), [7] overflow items, [8] prep CTAs done seeding
+                    // (overlapped attend), [7] overflow items
   int* group_done;  // [B*Hkv] right after counters: chunk publications per (seq, kv head)
   int* cnt;         // [chunks*G*4] candidate counts per scan sub-list (see CandList)
   int* selcnt;      // [chunks*G]

@@ -142,7 +142,7 @@ StageSet pick_g(int G) {
 bool tc_scan_eligible(const Batch& bt, int dtype, const alaya_seq* seqs);
 int launch_tc_scan(const Batch& bt, const alaya_seq* seqs, const float* q, const Ws& ws,
                    cudaStream_t st);
-bool overlap_enabled(int groups);
+bool overlap_enabled();
 int64_t diprs_row_bytes(int max_n, int cap);
 int launch_diprs(const Batch& bt, int dtype, const alaya_graph* graphs, const float* q, int l0, int floor_mode,
                  const float* floors, int cap, int64_t* ids, int64_t out_cap, int32_t* count, int32_t* explored,

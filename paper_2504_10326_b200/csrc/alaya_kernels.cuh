@@ -618,8 +618,14 @@ __global__ void __launch_bounds__(CW * 32)
   __shared__ int redn[CW];
   pdl_trigger();
   pdl_wait();
-  if (bt.call_id && threadIdx.x == 0)  // this call's prep has finished (async seeds)
-    while (ld_acquire_gpu(&ws.counters[8]) < bt.B * bt.Hkv) __nanosleep(64);
+  if (bt.call_id) {  // every prep CTA of this call is done seeding (none lands in a later call):
+    // its per-group flag carries this call's token (never zeroed, so a CTA whose header
+    // wait timed out still signs off -- a zeroed counter could lose that arrival)
+    const unsigned long long tok = call_token(bt);
+    for (int g = threadIdx.x; g < bt.B * bt.Hkv; g += blockDim.x)
+      while (ld_acquire_gpu_u64(ws.seeded + g) != tok) __nanosleep(64);
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int row = blockIdx.x;
   const int b = row / bt.Hq, qh = row - b * bt.Hq;
@@ -888,11 +894,9 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
       if (bt.seed && m > -INFINITY) atomicMax(&ws.gmax[b * bt.Hq + h * G + threadIdx.x], enc_max(m));
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0)  // seeds of this group are in (the scan's epilogue and combine wait on it)
       asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ws.seeded + blockIdx.x), "l"(call_token(bt))
                    : "memory");
-      asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(&ws.counters[8]), "r"(1) : "memory");
-    }
     return;
   }
   if (threadIdx.x < G) {

@@ -123,14 +123,11 @@ bool pdl_enabled() {
   return on != 0;
 }
 
-// attend beside the scan: ALAYA_OVERLAP=0 off, 1 on, default (-1) on when the
-// call has >= 32 (sequence, kv head) groups (measured at 128K: +8% at 4-8
-// sessions of 8 kv heads, neutral to -1% at 1-2 sessions)
-bool overlap_enabled(int groups) {
-  static const int mode = env_int("ALAYA_OVERLAP", -1);
-  // on by default since the async prep / combine changes (v16): B=1 89.0 -> 86.1 us,
-  // B=2 132.7 -> 129.0, 8K ctx B=4 55.9 -> 51.6 (tools/probe_latency.py)
-  (void)groups;
+// attend beside the scan: on for every tcgen05 call (ALAYA_OVERLAP=0 turns it
+// off). On since the async prep / combine changes (v16): B=1 89.0 -> 86.1 us,
+// B=2 132.7 -> 129.0, 8K ctx B=4 55.9 -> 51.6 (tools/probe_latency.py)
+bool overlap_enabled() {
+  static const int mode = env_int("ALAYA_OVERLAP", 1);
   return mode != 0;
 }
 

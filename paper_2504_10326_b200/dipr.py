@@ -2,7 +2,9 @@
 
 ``dipr_bruteforce`` runs the scan + exact-filter stages of the C-ABI over a
 single (q, keys) pair; the batched decode path lives in :mod:`.store`.
-The graph search (``diprs``/``traverse``/``CandidateList``) is out of scope.
+The graph search (``diprs``, ``dipr.py:107-289``) runs on the device as
+``alaya_diprs`` (decision-identical walk over a ``GraphIndex``); only graph
+CONSTRUCTION (``index.py:245-639``) is out of scope.
 """
 
 from __future__ import annotations

@@ -127,15 +127,21 @@ def seq_array(seqs: list[SeqView], params: AlayaParams, dtype: torch.dtype):
 
 
 class _Workspace(threading.local):
-    def __init__(self):
-        self.buf: dict[int, torch.Tensor] = {}
+    """Shared call workspaces, one per (device, stream): the kernels of one call
+    hand off through the workspace header (prep zeroes it while the previous
+    call's combine may still read it), which is only safe in stream order."""
 
-    def get(self, nbytes: int, device: torch.device) -> torch.Tensor:
+    def __init__(self):
+        self.buf: dict[tuple[int, int], torch.Tensor] = {}
+
+    def get(self, nbytes: int, device: torch.device, stream: int | None = None) -> torch.Tensor:
         idx = device.index if device.index is not None else torch.cuda.current_device()
-        t = self.buf.get(idx)
+        if stream is None:
+            stream = torch.cuda.current_stream(device).cuda_stream
+        t = self.buf.get((idx, stream))
         if t is None or t.numel() < nbytes:
             t = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
-            self.buf[idx] = t
+            self.buf[(idx, stream)] = t
         return t
 
 
@@ -159,9 +165,28 @@ class Call:
         nbytes = self.lib.alaya_workspace_bytes(ctypes.byref(params), self.seqs, self.B)
         if nbytes == 0:
             check(_lib.ALAYA_ERR_ARG)
-        self.ws = ws if ws is not None and ws.numel() >= nbytes else _WS.get(nbytes, device)
-        self.ws_bytes = self.ws.numel()
+        self._nbytes = nbytes
+        self._ws_stream = torch.cuda.current_stream(device).cuda_stream
+        self._ws_shared = not (ws is not None and ws.numel() >= nbytes)
+        self._ws = _WS.get(nbytes, device, self._ws_stream) if self._ws_shared else ws
+        self.ws_bytes = self._ws.numel()
         self._dtype = dtype
+
+    @property
+    def ws(self) -> torch.Tensor:
+        """The call's workspace. A shared (cached) workspace belongs to one stream: a
+        call issued on another stream switches to that stream's workspace, so two
+        streams never race on one header."""
+        if self._ws_shared:
+            st = torch.cuda.current_stream(self.device).cuda_stream
+            if st != self._ws_stream:
+                self._ws = _WS.get(self._nbytes, self.device, st)
+                self._ws_stream, self.ws_bytes = st, self._ws.numel()
+        return self._ws
+
+    @ws.setter
+    def ws(self, t: torch.Tensor) -> None:  # a caller-owned workspace (e.g. a captured graph's)
+        self._ws, self._ws_shared, self.ws_bytes = t, False, t.numel()
 
     @property
     def stream(self) -> int:

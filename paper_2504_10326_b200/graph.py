@@ -58,8 +58,12 @@ class DecodeStepGraph:
             c.ws, c.ws_bytes = self.ws, self.ws.numel()
         self.appends = [engine.append_array(l, params, dtype) for l in layers]
         self.counters = [s.w_dev for l in layers for s in l]
+        # every replay appends one row to every ring: the device append kernel drops a
+        # row once the ring is full, so the host refuses that replay instead
+        self.capacity = min(int(sv.wk.shape[1]) for l in layers for sv in l)
         self.graph = torch.cuda.CUDAGraph()
         self._capture()
+        self.sync_rows()
 
     def _step(self) -> None:
         self.seq.add_(1)
@@ -81,7 +85,26 @@ class DecodeStepGraph:
             self._step()
         torch.cuda.synchronize(self.device)
 
+    def sync_rows(self) -> int:
+        """Re-read the device window row counts (after the caller changed them) and
+        return the fullest ring's row count."""
+        self.rows = int(torch.stack([c[:1] for c in self.counters]).max().item())
+        return self.rows
+
+    @property
+    def remaining(self) -> int:
+        """Replays left before the fullest window ring is at capacity."""
+        return self.capacity - self.rows
+
     def replay(self) -> torch.Tensor:
-        """One decode step of every layer (stream-ordered); returns :attr:`out`."""
+        """One decode step of every layer (stream-ordered); returns :attr:`out`.
+
+        Raises ``RuntimeError`` when a ring has no free row left (the reference's
+        ``Session.update`` always appends, ``store.py:160-189``; the captured ring
+        cannot grow): re-create the step with larger rings."""
+        if self.rows >= self.capacity:
+            raise RuntimeError(f"decode-step graph: window ring full ({self.rows}/{self.capacity} rows); "
+                               "re-capture with a larger ring")
         self.graph.replay()
+        self.rows += 1
         return self.out

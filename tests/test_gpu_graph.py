@@ -83,3 +83,24 @@ def test_graph_mode_append_stops_at_capacity(cuda_ok):
     assert int(cnt.item()) == 3  # row 2 written, then the ring is full
     assert torch.all(wk[:, 2] == 1.0) and torch.all(wv[:, 2] == -1.0)
     assert torch.all(wk[:, :2] == 0)
+
+
+def test_graph_replay_refuses_a_full_ring(cuda_ok):
+    """the device append drops rows at capacity, so DecodeStepGraph.replay
+    must refuse the replay that would need a row the ring does not have."""
+    from paper_2504_10326_b200 import DecodeStepGraph, engine
+    L, B, hq, hkv, d, n, cap, w0 = 1, 1, 8, 2, 128, 3000, 5, 2
+    dev, K, V, WK, WV = _setup(L, B, hq, hkv, d, n, cap, w0, 3)
+    params = engine.make_params(hq, hkv, d, torch.bfloat16, 20.0, 16, 64)
+    counts = [torch.full((1,), w0, dtype=torch.int32, device=dev)]
+    layers = [[engine.SeqView(k=K[0][0], v=V[0][0], n=n, wk=WK[0, 0], wv=WV[0, 0], w_dev=counts[0])]]
+    gr = DecodeStepGraph(layers, params, torch.bfloat16, dev)
+    assert gr.remaining == cap - w0
+    for _ in range(cap - w0):
+        gr.replay()
+    torch.cuda.synchronize()
+    assert int(counts[0].item()) == cap and gr.remaining == 0
+    with pytest.raises(RuntimeError, match="window ring full"):
+        gr.replay()
+    counts[0].fill_(w0)  # the caller rewinds the ring: re-read the counts
+    assert gr.sync_rows() == w0 and gr.remaining == cap - w0

@@ -169,3 +169,13 @@ def test_diprs_complete_graph_is_exact(rng):
     off = np.arange(0, 12 * 11 + 1, 11)
     for beta in (0.0, 2.0, 10.0):
         assert O.diprs(keys, off, nb, q, 0, 16, beta) == O.dipr_bruteforce(q, keys, beta)
+
+
+def test_package_alpha_to_beta_matches_oracle():
+    """The package's host formula (dipr.py:29-39) against the pinned oracle's copy."""
+    from paper_2504_10326_b200 import dipr as D
+    for alpha, d in ((1.0, 128), (np.exp(-2.0), 64), (0.05, 128), (1e-6, 16)):
+        assert D.alpha_to_beta(alpha, d) == pytest.approx(O.alpha_to_beta(alpha, d), rel=1e-15)
+    for bad in ((0.0, 8), (1.5, 8), (0.5, 0)):
+        with pytest.raises(ValueError):
+            D.alpha_to_beta(*bad)

@@ -8,9 +8,11 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from paper_2504_10326_b200 import _lib  # noqa: E402
+import subprocess  # noqa: E402
 
-lib = _lib.load()
+_DIAG = os.path.join(os.path.dirname(os.path.abspath(__file__)), "diag")
+subprocess.run(["make", "-C", _DIAG], check=True)  # probes live outside the product .so
+lib = ctypes.CDLL(os.path.join(_DIAG, "libalaya_diag.so"))
 lib.alaya_diag_read.restype = ctypes.c_int
 lib.alaya_diag_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p,
                                 ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
