@@ -128,6 +128,10 @@ typedef struct {
 
 const char* alaya_last_error(void);
 int alaya_version(void);
+/* Diagnostics only (not a reference interface): while d_buf is non-null, the
+ * prep/scan/attend/combine kernels of every later call stamp %globaltimer per
+ * CTA into d_buf as u64 [4 kinds][1024 CTAs][16 slots] (needs 512 KB). */
+int alaya_debug_trace(void* d_buf, int64_t bytes);
 
 /* Workspace bytes needed for a call on this batch. */
 size_t alaya_workspace_bytes(const alaya_params* p, const alaya_seq* seqs, int batch);

@@ -42,7 +42,7 @@ EXPORTS = (
     "alaya_sparse_attention", "alaya_avdb_stat", "alaya_avdb_write", "alaya_avdb_staging_bytes",
     "alaya_avdb_load", "alaya_avdb_graph", "alaya_diprs", "alaya_diprs_workspace_bytes",
     "alaya_exch_bytes", "alaya_exch_alloc", "alaya_exch_open", "alaya_exch_close", "alaya_exch_free",
-    "alaya_exch", "alaya_exch_slots",
+    "alaya_exch", "alaya_exch_slots", "alaya_debug_trace",
 )
 
 
@@ -126,6 +126,8 @@ def load() -> ctypes.CDLL:
     lib.alaya_last_error.restype = ctypes.c_char_p
     lib.alaya_last_error.argtypes = []
     lib.alaya_version.restype = i32
+    lib.alaya_debug_trace.restype = i32
+    lib.alaya_debug_trace.argtypes = [vp, ctypes.c_int64]
     lib.alaya_workspace_bytes.restype = sz
     lib.alaya_workspace_bytes.argtypes = [P, S, i32]
     lib.alaya_dipr_attention.restype = i32

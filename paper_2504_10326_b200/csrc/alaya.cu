@@ -36,6 +36,7 @@ int cuda_check(const char* what) {
 namespace {
 
 constexpr int kNumSMs = 148;
+unsigned long long* g_trace = nullptr;  // alaya_debug_trace
 
 bool dim_ok(int d) { return d == 16 || d == 32 || d == 64 || d == 128 || d == 256; }
 
@@ -129,6 +130,7 @@ int build_batch(const alaya_params* p, const alaya_seq* seqs, int B, Batch* bt) 
     cb += p->n_kv_heads * k.nch;
   }
   bt->total_chunks = cb;
+  bt->trace = g_trace;
   return ALAYA_OK;
 }
 
@@ -280,6 +282,13 @@ int run_scan(Call& c, const float* d_q, bool ends_in_combine = true) {
 extern "C" {
 
 const char* alaya_last_error(void) { return g_err.c_str(); }
+
+int alaya_debug_trace(void* d_buf, int64_t bytes) {
+  if (d_buf && bytes < (int64_t)4 * kTraceCtas * kTraceSlots * 8)
+    return fail(ALAYA_ERR_WORKSPACE, "trace buffer needs %d bytes", 4 * kTraceCtas * kTraceSlots * 8);
+  g_trace = static_cast<unsigned long long*>(d_buf);
+  return ALAYA_OK;
+}
 int alaya_version(void) { return 1; }
 
 size_t alaya_workspace_bytes(const alaya_params* p, const alaya_seq* seqs, int batch) {

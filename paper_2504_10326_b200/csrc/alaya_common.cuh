@@ -96,7 +96,29 @@ struct Batch {
                           // score) replacing max - beta in the scan; null for DIPR
   int32_t sx_on;          // fused sharded step (needs overlap): see ShardExch
   ShardExch sx;
+  unsigned long long* trace;  // diagnostics (alaya_debug_trace): per-CTA %globaltimer stamps or null
 };
+
+// Diagnostic timeline: trace[kind][cta][slot] = %globaltimer (ns). kinds: 0 prep,
+// 1 scan, 2 attend, 3 combine; slot 0 = CTA start, 1 = CTA end, 2.. = kind-specific.
+constexpr int kTraceCtas = 1024, kTraceSlots = 16;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_max(const Batch& bt, int kind, int slot, unsigned long long v) {
+  if (bt.trace && blockIdx.x < kTraceCtas && slot < kTraceSlots)
+    atomicMax(bt.trace + ((size_t)kind * kTraceCtas + blockIdx.x) * kTraceSlots + slot, v);
+}
+__device__ __forceinline__ void trace_add(const Batch& bt, int kind, int slot, unsigned long long v) {
+  if (bt.trace && blockIdx.x < kTraceCtas && slot < kTraceSlots)
+    atomicAdd(bt.trace + ((size_t)kind * kTraceCtas + blockIdx.x) * kTraceSlots + slot, v);
+}
+__device__ __forceinline__ void trace_rec(const Batch& bt, int kind, int slot) {
+  if (bt.trace && blockIdx.x < kTraceCtas && slot < kTraceSlots)
+    bt.trace[((size_t)kind * kTraceCtas + blockIdx.x) * kTraceSlots + slot] = gtimer();
+}
 
 // Coarse block indexes of a batch (kernel-parameter space).
 struct BixSet {

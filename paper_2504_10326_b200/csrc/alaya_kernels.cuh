@@ -546,6 +546,7 @@ __global__ void __launch_bounds__(kOvlThreads, 4)  // <= 128 regs: one CTA fits 
   __shared__ int s_t[W][2][32];
   __shared__ float s_w[W][2][32];
   pdl_trigger();
+  if (threadIdx.x == 0) trace_rec(bt, 2, 0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwin = bt.B * bt.Hq;
   const int npairs = bt.total_chunks * G;
@@ -575,6 +576,7 @@ __global__ void __launch_bounds__(kOvlThreads, 4)  // <= 128 regs: one CTA fits 
         __syncwarp();
       }
       qe = __ldcg(&ws.heavy[cj]) ? 1 : 4;
+      if (bt.trace && lane == 0) trace_max(bt, 2, 2, gtimer());  // latest group-ready of a pair task
     } else {
       if (novl < 0) {  // overflow items are final once every chunk has published
         if (lane == 0) {
@@ -594,8 +596,19 @@ __global__ void __launch_bounds__(kOvlThreads, 4)  // <= 128 regs: one CTA fits 
         sx_global_max(bt, ws, b, h, (int)(cj - (cj / G) * G), lane);
       }
     }
+    const unsigned long long t_task = bt.trace ? gtimer() : 0ull;
     sel_task_pipe<T, D, G, true>(bt, bt.sx_on ? ws.smaxbuf : nullptr, ws, cj, qb, qe, lane, s_t[warp],
                                  s_w[warp], true);
+    if (bt.trace && lane == 0) {
+      const unsigned long long t1 = gtimer();
+      trace_max(bt, 2, 3, t1);                 // last task end
+      trace_max(bt, 2, 4, t1 - t_task);        // longest task (ns)
+      atomicAdd(bt.trace + ((size_t)2 * kTraceCtas + min((int)blockIdx.x, kTraceCtas - 1)) * kTraceSlots + 5, 1ull);
+    }
+  }
+  if (bt.trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) trace_rec(bt, 2, 1);
   }
 }
 
@@ -617,6 +630,7 @@ __global__ void __launch_bounds__(CW * 32)
   __shared__ float redl[CW];
   __shared__ int redn[CW];
   pdl_trigger();
+  if (threadIdx.x == 0) trace_rec(bt, 3, 0);
   pdl_wait();
   if (bt.call_id) {  // every prep CTA of this call is done seeding (none lands in a later call):
     // its per-group flag carries this call's token (never zeroed, so a CTA whose header
@@ -626,6 +640,7 @@ __global__ void __launch_bounds__(CW * 32)
       while (ld_acquire_gpu_u64(ws.seeded + g) != tok) __nanosleep(64);
     __syncthreads();
   }
+  if (threadIdx.x == 0) trace_rec(bt, 3, 2);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int row = blockIdx.x;
   const int b = row / bt.Hq, qh = row - b * bt.Hq;
@@ -727,6 +742,7 @@ __global__ void __launch_bounds__(CW * 32)
       }
     }
   }
+  if (lane == 0) trace_rec(bt, 3, 1);
   if (bt.sx_on && bt.sx.gepoch) {  // last row out raises this rank's kind-1 flag everywhere
     const ShardExch& x = bt.sx;
     __threadfence_system();
@@ -777,13 +793,52 @@ template <typename T, int D, int G>
 __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ Batch bt,
                                                         const float* __restrict__ q, Ws ws) {
   constexpr int DL = (D + 31) / 32;
+  constexpr int RU = kPrepSamples / kWarps;  // rows in flight per warp
   __shared__ float red[kWarps][G];
   pdl_trigger();
-  pdl_wait();
+  if (threadIdx.x == 0) trace_rec(bt, 0, 0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.x / bt.Hkv, h = blockIdx.x - b * bt.Hkv;
   const KSeq& s = bt.s[b];
   const bool async = bt.call_id != 0;
+  const int S = min(s.n, kPrepSamples);
+  const T* kb = reinterpret_cast<const T*>(s.k) + (size_t)h * s.hs;
+  // + the base window ids this shard holds (core.py:159-165): real base tokens, and
+  // the recent ones are often in the query's cluster
+  const int64_t P = s.P, off = s.off;
+  int64_t a0 = 0, a1, b0, b1;
+  if (P <= (int64_t)bt.wi + bt.wl) { a1 = P; b0 = 0; b1 = 0; }
+  else { a1 = bt.wi; b0 = P - bt.wl; b1 = P; }
+  a0 = max(a0, off) - off; a1 = min(a1, off + s.n) - off; if (a1 < a0) a1 = a0;
+  b0 = max(b0, off) - off; b1 = min(b1, off + s.n) - off; if (b1 < b0) b1 = b0;
+  const int na = (int)(a1 - a0), nbw = (int)(b1 - b0);
+  // window rows join the sample only when the block filter consumes the seed (they
+  // tighten its LB; otherwise the extra load rounds cost more than they save)
+  const int R = bt.seed ? S + (bt.block_filter ? min(na + nbw, 2 * kPrepSamples) : 0) : 0;
+  float x[RU][DL];
+  auto load_round = [&](int i0) {
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      const int i = i0 + u;
+      int64_t row = 0;
+      if (i < S) row = (int64_t)i * s.n / S;
+      else if (i - S < na) row = a0 + (i - S);
+      else row = b0 + (i - S - na);
+      const T* kr = kb + (size_t)row * D;
+#pragma unroll
+      for (int k = 0; k < DL; ++k) {
+        const int e = lane + 32 * k;
+        x[u][k] = (i < R && e < D) ? to_f(kr[e]) : 0.f;
+      }
+    }
+  };
+  // the first sampled rows are loaded BEFORE the grid-dependency wait: K is context
+  // memory, never written by the kernels this call follows (the scan's TMA producer
+  // relies on the same), so their HBM latency overlaps the previous call's tail
+  int i0 = warp * RU;
+  if (i0 < R) load_round(i0);
+  pdl_wait();
+  if (threadIdx.x == 0) trace_rec(bt, 0, 2);
   if (async) {  // CTA 0 zeroes the whole header, then publishes it (the scan waits on ws.ready)
     if (blockIdx.x == 0) {
       const int rows = bt.B * bt.Hq;
@@ -804,15 +859,15 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
     if (threadIdx.x == 0) ws.group_done[blockIdx.x] = 0;
   }
   if (bt.sx_on && s.nch == 0) {  // fused sharded step: no chunk will complete this group
-    const ShardExch& x = bt.sx;
-    const int parity = (int)(x.epoch & 1ull);
-    if (threadIdx.x < G * x.R) {
+    const ShardExch& sx = bt.sx;
+    const int parity = (int)(sx.epoch & 1ull);
+    if (threadIdx.x < G * sx.R) {
       const int j = threadIdx.x % G, r = threadIdx.x / G;
-      exch_slot(x.peers[r], parity, 0, x.rank, x.R, x.cap)[b * bt.Hq + h * G + j] = -INFINITY;
+      exch_slot(sx.peers[r], parity, 0, sx.rank, sx.R, sx.cap)[b * bt.Hq + h * G + j] = -INFINITY;
     }
     __threadfence_system();
     __syncthreads();
-    if (threadIdx.x < x.R) st_release_sys_u64(exch_gflag(x.peers[threadIdx.x], blockIdx.x, x.rank), x.epoch);
+    if (threadIdx.x < sx.R) st_release_sys_u64(exch_gflag(sx.peers[threadIdx.x], blockIdx.x, sx.rank), sx.epoch);
   }
   float qr[G][DL];
 #pragma unroll
@@ -825,37 +880,8 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
   float best[G];
 #pragma unroll
   for (int j = 0; j < G; ++j) best[j] = -INFINITY;
-  const int S = min(s.n, kPrepSamples);
-  const T* kb = reinterpret_cast<const T*>(s.k) + (size_t)h * s.hs;
-  // + the base window ids this shard holds (core.py:159-165): real base tokens, and
-  // the recent ones are often in the query's cluster
-  const int64_t P = s.P, off = s.off;
-  int64_t a0 = 0, a1, b0, b1;
-  if (P <= (int64_t)bt.wi + bt.wl) { a1 = P; b0 = 0; b1 = 0; }
-  else { a1 = bt.wi; b0 = P - bt.wl; b1 = P; }
-  a0 = max(a0, off) - off; a1 = min(a1, off + s.n) - off; if (a1 < a0) a1 = a0;
-  b0 = max(b0, off) - off; b1 = min(b1, off + s.n) - off; if (b1 < b0) b1 = b0;
-  const int na = (int)(a1 - a0), nbw = (int)(b1 - b0);
-  // window rows join the sample only when the block filter consumes the seed (they
-  // tighten its LB; otherwise the extra load rounds cost more than they save)
-  const int R = bt.seed ? S + (bt.block_filter ? min(na + nbw, 2 * kPrepSamples) : 0) : 0;
-  constexpr int RU = kPrepSamples / kWarps;  // rows in flight per warp
-  for (int i0 = warp * RU; i0 < R; i0 += kWarps * RU) {
-    float x[RU][DL];
-#pragma unroll
-    for (int u = 0; u < RU; ++u) {
-      const int i = i0 + u;
-      int64_t row = 0;
-      if (i < S) row = (int64_t)i * s.n / S;
-      else if (i - S < na) row = a0 + (i - S);
-      else row = b0 + (i - S - na);
-      const T* kr = kb + (size_t)row * D;
-#pragma unroll
-      for (int k = 0; k < DL; ++k) {
-        const int e = lane + 32 * k;
-        x[u][k] = (i < R && e < D) ? to_f(kr[e]) : 0.f;
-      }
-    }
+  for (; i0 < R; i0 += kWarps * RU) {
+    if (i0 != warp * RU) load_round(i0);
 #pragma unroll
     for (int u = 0; u < RU; ++u) {
 #pragma unroll
@@ -876,7 +902,7 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
 #pragma unroll
     for (int j = 0; j < G; ++j) red[warp][j] = best[j];
   __syncthreads();
-  if (async) {  // seeds join the running max once the header is zeroed; then count this CTA done
+  if (async) {  // seeds join the running max once the header is zeroed
     __shared__ int s_ok;
     if (threadIdx.x == 0) {
       // bounded: a seed is optional (a lower bound), so a CTA that cannot see the
@@ -894,9 +920,11 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
       if (bt.seed && m > -INFINITY) atomicMax(&ws.gmax[b * bt.Hq + h * G + threadIdx.x], enc_max(m));
     }
     __syncthreads();
-    if (threadIdx.x == 0)  // seeds of this group are in (the scan's epilogue and combine wait on it)
+    if (threadIdx.x == 0) {  // seeds of this group are in (combine waits on it)
       asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ws.seeded + blockIdx.x), "l"(call_token(bt))
                    : "memory");
+      trace_rec(bt, 0, 1);
+    }
     return;
   }
   if (threadIdx.x < G) {

@@ -51,12 +51,8 @@ int launch_s(const Batch& bt, const tc::Maps& maps, const float* q, const Ws& ws
              int ctas_per_sm) {
   const size_t sm = tc::tc_smem_bytes(G, S);
   cudaFuncSetAttribute(tc::scan_tc_kernel<G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  // equal chunk counts per CTA: ceil(chunks / rounds) CTAs, rounds = ceil(chunks /
-  // resident slots), so no tail round runs a fraction of the grid
-  const int slots = ctas_per_sm * num_sms();
-  const int rounds = (bt.total_chunks + slots - 1) / slots;
-  static const int balance = env_int("ALAYA_TC_BALANCE", 1);
-  const int grid = balance ? (bt.total_chunks + rounds - 1) / rounds : std::min(bt.total_chunks, slots);
+  // persistent: every resident slot, chunks handed out dynamically (scan_tc_kernel)
+  const int grid = std::min(bt.total_chunks, ctas_per_sm * num_sms());
   return launch_pdl("scan_tc_kernel", tc::scan_tc_kernel<G, S>, grid, tc::kThreadsTc, sm, st, bt, maps, q, ws);
 }
 
@@ -65,7 +61,7 @@ int launch_s(const Batch& bt, const tc::Maps& maps, const float* q, const Ws& ws
 // 1 CTA uses ALAYA_TC_STAGES (4..6, default 6).
 template <int G>
 int launch(const Batch& bt, const tc::Maps& maps, const float* q, const Ws& ws, cudaStream_t st) {
-  static const int ctas = env_int("ALAYA_TC_CTAS", 3);
+  static const int ctas = env_int("ALAYA_TC_CTAS", 2);
   static const int stages = env_int("ALAYA_TC_STAGES", 6);
   if (ctas >= 3) return launch_s<G, 2>(bt, maps, q, ws, st, 3);
   if (ctas == 2) return launch_s<G, 3>(bt, maps, q, ws, st, 2);
