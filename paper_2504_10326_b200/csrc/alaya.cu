@@ -140,7 +140,7 @@ struct Layout {
   size_t zero_bytes;
   size_t cscore_end;
   size_t status, seeded, gmax, counters, cnt, selcnt, retcnt, part_l, part_acc, cidx, cscore, partbuf, smaxbuf,
-      keep, ovl_l, ovl_acc, ovl_sel, ovl_ret, heavy, ovlist, total;
+      keep, ovl_l, ovl_acc, ovl_sel, ovl_ret, heavy, ovlist, gidx, total;
 };
 
 Layout layout_for(const Batch& bt) {
@@ -169,6 +169,7 @@ Layout layout_for(const Batch& bt) {
   L.partbuf = o; o = align_up(o + 4 * rows * (D + 2));
   L.smaxbuf = o; o = align_up(o + 4 * rows);
   L.keep = o; o = align_up(o + 8 * C);
+  L.gidx = o; o = align_up(o + 4 * C * bt.chunk);
   L.total = o;
   return L;
 }
@@ -177,6 +178,8 @@ Ws carve(const Layout& L, void* base) {
   char* c = static_cast<char*>(base);
   Ws w;
   w.status = reinterpret_cast<int*>(c + L.status);
+  w.mode = w.status + 1;
+  w.gidx = reinterpret_cast<int*>(c + L.gidx);
   w.ready = reinterpret_cast<unsigned long long*>(c + L.status + 8);
   w.seeded = reinterpret_cast<unsigned long long*>(c + L.seeded);
   w.gmax = reinterpret_cast<uint32_t*>(c + L.gmax);
@@ -369,12 +372,15 @@ int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch
   if (!d_q || !d_out) return fail(ALAYA_ERR_ARG, "null q/out");
   for (int b = 0; b < batch; ++b)
     if (seqs[b].prefix_len + seqs[b].w == 0) return fail(ALAYA_ERR_ARG, "attention on an empty session");
+  c.bt.win_in_prep = 1;  // window partials computed by prep, off the attend's tail
   // attend beside the scan (per-group readiness); the CUDA-core scan fills the
   // register file (no room for an attend CTA: measured no gain), so tcgen05 only
   if (c.use_tc && overlap_enabled()) {
     c.bt.overlap = 1;
+    c.bt.gfmt = gfmt_enabled(c.bt);
     if ((rc = run_scan(c, d_q))) return rc;
-    if ((rc = c.st.attend_ovl(c.bt, d_q, c.ws, c.stream))) return rc;
+    if ((rc = c.bt.gfmt ? c.st.attend_grp(c.bt, d_q, c.ws, c.stream) : c.st.attend_ovl(c.bt, d_q, c.ws, c.stream)))
+      return rc;
     return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);
   }
   if ((rc = run_scan(c, d_q))) return rc;  // prep zeroed the status word and the ticket
@@ -402,6 +408,8 @@ int alaya_sharded_step(const alaya_params* p, const alaya_seq* seqs, int batch, 
     if (!bufs[r]) return fail(ALAYA_ERR_ARG, "null peer buffer %d", r);
   c.bt.overlap = 1;
   c.bt.sx_on = 1;
+  c.bt.win_in_prep = 1;
+  c.bt.gfmt = gfmt_enabled(c.bt);
   for (int r = 0; r < n_ranks; ++r) c.bt.sx.peers[r] = static_cast<char*>(bufs[r]);
   c.bt.sx.rank = rank;
   c.bt.sx.R = n_ranks;
@@ -410,7 +418,8 @@ int alaya_sharded_step(const alaya_params* p, const alaya_seq* seqs, int batch, 
   c.bt.sx.gepoch = gather_epoch;
   c.bt.sx.err = d_err;
   if ((rc = run_scan(c, d_q))) return rc;
-  if ((rc = c.st.attend_ovl(c.bt, d_q, c.ws, c.stream))) return rc;
+  if ((rc = c.bt.gfmt ? c.st.attend_grp(c.bt, d_q, c.ws, c.stream) : c.st.attend_ovl(c.bt, d_q, c.ws, c.stream)))
+    return rc;
   return c.st.combine(c.bt, c.ws.smaxbuf, c.ws, nullptr, d_part, nullptr, c.stream);
 }
 
@@ -481,7 +490,7 @@ int alaya_selected(const alaya_params* p, const alaya_seq* seqs, int batch, int6
   if (rc) return rc;
   if (!d_ids || !d_selected || !d_retrieved) return fail(ALAYA_ERR_ARG, "null outputs");
   selected_kernel<<<batch * c.bt.Hq, kThreads, 0, c.stream>>>(c.bt, c.ws, d_ids, cap, d_selected,
-                                                              d_retrieved);
+                                                              d_retrieved);  // (format: ws.mode)
   return cuda_check("selected_kernel");
 }
 

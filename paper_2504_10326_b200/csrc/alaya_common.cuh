@@ -97,6 +97,10 @@ struct Batch {
   int32_t sx_on;          // fused sharded step (needs overlap): see ShardExch
   ShardExch sx;
   unsigned long long* trace;  // diagnostics (alaya_debug_trace): per-CTA %globaltimer stamps or null
+  int32_t win_in_prep;  // prep_kernel computes the window partials (the attend skips window tasks)
+  int32_t gfmt;         // group candidate format: the tcgen05 scan writes one list per (chunk,
+                        // quarter) of rows some head of the GQA group keeps, with all G scores;
+                        // attend_grp_kernel gathers each V row once for the whole group
 };
 
 // Diagnostic timeline: trace[kind][cta][slot] = %globaltimer (ns). kinds: 0 prep,
@@ -135,6 +139,8 @@ __device__ __forceinline__ unsigned long long call_token(const Batch& bt) {
 
 struct Ws {
   int* status;
+  int* mode;        // status + 1: candidate format of the call (1 = group format), set by prep
+  int* gidx;        // [chunks][chunk] group format: candidate rows per (chunk, quarter) sub-list
   unsigned long long* ready;  // call id whose header prep has zeroed (next to status, never zeroed)
   unsigned long long* seeded;  // [B*Hkv] call id whose seeds of (seq, kv head) are in gmax (never zeroed)
   uint32_t* gmax;   // [B*Hq] order-preserving encoded running max

@@ -48,12 +48,21 @@ struct Stages {
     return launch_pdl("scan_kernel", scan_kernel<T, D, G>, bt.total_chunks, kThreads, sm, st, bt, q, ws);
   }
   static int prep(const Batch& bt, const float* q, const Ws& ws, cudaStream_t st) {
-    return launch_pdl("prep_kernel", prep_kernel<T, D, G>, bt.B * bt.Hkv, kThreads, 0, st, bt, q, ws);
+    // window partials in prep: one (m, l, acc) staging row per (warp, head)
+    const size_t sm = bt.win_in_prep ? (size_t)kWarps * G * (D + 2) * 4 : 0;
+    if (sm > 48 * 1024) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(prep_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        attr = true;
+      }
+    }
+    return launch_pdl("prep_kernel", prep_kernel<T, D, G>, bt.B * bt.Hkv, kThreads, sm, st, bt, q, ws);
   }
   // zero_ticket = 0: the ticket was zeroed by prep_kernel in this call
   static int attend(const Batch& bt, const float* q, const float* smax, const Ws& ws,
                     int want_values, cudaStream_t st, int zero_ticket = 1) {
-    const long tasks = (long)bt.total_chunks * G + (want_values ? (long)bt.B * bt.Hq : 0);
+    const long tasks = (long)bt.total_chunks * G + ((want_values && !bt.win_in_prep) ? (long)bt.B * bt.Hq : 0);
     if (tasks == 0) return ALAYA_OK;
     static int per_sm = 0;
     if (per_sm == 0) {
@@ -74,10 +83,23 @@ struct Stages {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attend_ovl_kernel<T, D, G>, kOvlThreads, 0);
       if (per_sm < 1) per_sm = 1;
     }
-    const long tasks = (long)bt.total_chunks * G + (long)bt.B * bt.Hq;
+    const long tasks = (long)bt.total_chunks * G + (bt.win_in_prep ? 0 : (long)bt.B * bt.Hq);
     const long blocks = std::min<long>((tasks + 3) / 4, (long)per_sm * num_sms());
     return launch_pdl("attend_ovl_kernel", attend_ovl_kernel<T, D, G>, (unsigned)blocks, kOvlThreads, 0,
                       st, bt, q, ws);
+  }
+  // group-format attend beside the tcgen05 scan: one 4-warp CTA per chunk
+  static int attend_grp(const Batch& bt, const float* q, const Ws& ws, cudaStream_t st) {
+    (void)q;
+    static int per_sm = 0;
+    if (per_sm == 0) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attend_grp_kernel<T, D, G>, kGrpThreads, 0);
+      if (per_sm < 1) per_sm = 1;
+    }
+    const long blocks = std::min<long>(bt.total_chunks, (long)per_sm * num_sms());
+    if (blocks == 0) return ALAYA_OK;
+    return launch_pdl("attend_grp_kernel", attend_grp_kernel<T, D, G>, (unsigned)blocks, kGrpThreads, 0, st, bt,
+                      ws);
   }
   static int filter(const Batch& bt, const float* q, const Ws& ws, cudaStream_t st) {
     if (bt.total_chunks == 0) return ALAYA_OK;
@@ -112,12 +134,14 @@ struct StageSet {
   FilterFn filter;
   ScanFn prep;
   ScanFn attend_ovl;
+  ScanFn attend_grp;
 };
 
 template <typename T, int D, int G>
 StageSet make_set() {
   return {&Stages<T, D, G>::scan, &Stages<T, D, G>::attend, &Stages<T, D, G>::combine,
-          &Stages<T, D, G>::filter, &Stages<T, D, G>::prep, &Stages<T, D, G>::attend_ovl};
+          &Stages<T, D, G>::filter, &Stages<T, D, G>::prep, &Stages<T, D, G>::attend_ovl,
+          &Stages<T, D, G>::attend_grp};
 }
 
 template <typename T, int D>
@@ -143,6 +167,7 @@ bool tc_scan_eligible(const Batch& bt, int dtype, const alaya_seq* seqs);
 int launch_tc_scan(const Batch& bt, const alaya_seq* seqs, const float* q, const Ws& ws,
                    cudaStream_t st);
 bool overlap_enabled();
+bool gfmt_enabled(const Batch& bt);
 int64_t diprs_row_bytes(int max_n, int cap);
 int launch_diprs(const Batch& bt, int dtype, const alaya_graph* graphs, const float* q, int l0, int floor_mode,
                  const float* floors, int cap, int64_t* ids, int64_t out_cap, int32_t* count, int32_t* explored,

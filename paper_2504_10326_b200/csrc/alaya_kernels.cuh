@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   pdl_trigger();
   pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nwin = want_values ? bt.B * bt.Hq : 0;
+  const int nwin = (want_values && !bt.win_in_prep) ? bt.B * bt.Hq : 0;
   const int npairs = bt.total_chunks * G;
   // + overflow items published by the scan (none without chunks: no scan ran)
   const int ntasks = nwin + npairs + (npairs ? ws.counters[7] : 0);
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(kOvlThreads, 4)  // <= 128 regs: one CTA fits 
   pdl_trigger();
   if (threadIdx.x == 0) trace_rec(bt, 2, 0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nwin = bt.B * bt.Hq;
+  const int nwin = bt.win_in_prep ? 0 : bt.B * bt.Hq;
   const int npairs = bt.total_chunks * G;
   const int all_done = 4 * bt.total_chunks;
   int novl = -1;
@@ -612,6 +612,187 @@ __global__ void __launch_bounds__(kOvlThreads, 4)  // <= 128 regs: one CTA fits 
   }
 }
 
+// Group-format attend (bt.gfmt; reference: dipr.py:64 filter, store.py:271-278,
+// attention.py:98-110). One 4-warp CTA per chunk: warp q walks the chunk's
+// quarter-q list of rows some head of the GQA group may keep (with all G
+// scores, written by the tcgen05 scan), applies every head's exact filter
+// s_j >= gmax_j - beta minus the window ids, and gathers each kept V row ONCE
+// for the whole group (G weighted sums per row), so V rows the G heads share
+// are not re-read. The 4 quarter partials are summed in fixed order into one
+// (chunk, head) partial; per-quarter selected ids go to the per-head lists for
+// diagnostics (alaya_selected). Launched beside the scan like attend_ovl_kernel:
+// a chunk starts once its (sequence, kv head) group has published every chunk.
+// It pays G FMAs per gathered row, so it wins only when the heads share most of
+// their rows (high beta): see gfmt_enabled().
+constexpr int kGrpThreads = 128;
+
+template <typename T, int D, int G>
+__global__ void __launch_bounds__(kGrpThreads, 4)
+    attend_grp_kernel(const __grid_constant__ Batch bt, Ws ws) {
+  constexpr int DPL = D >= 16 ? D / 16 : 1;  // (the group format runs at d = 128 only)
+  constexpr int U = G <= 4 ? 16 : 8;         // V rows in flight per half-warp
+  __shared__ int s_task;
+  __shared__ int s_row[4][32];
+  __shared__ float s_w[4][G][32];
+  __shared__ float s_red[3][D >= 16 ? D : 16];
+  __shared__ float s_l[4][G];
+  __shared__ int s_ns[4][G], s_nr[4][G];
+  pdl_trigger();
+  if (threadIdx.x == 0) trace_rec(bt, 2, 0);
+  if constexpr (D < 16) {
+    return;
+  } else {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, hl = lane & 15, half = lane >> 4;
+  const int chunk = bt.chunk, qcap = chunk / 4;
+  const float k2 = bt.inv_sqrt_d * kLog2e;
+  for (;;) {
+    __syncthreads();  // s_task / s_* of the previous task are consumed
+    if (threadIdx.x == 0) s_task = atomicAdd(&ws.counters[0], 1);
+    __syncthreads();
+    const int c = s_task;
+    if (c >= bt.total_chunks) break;
+    int b, h, ci;
+    decode_chunk(bt, c, b, h, ci);
+    const KSeq& s = bt.s[b];
+    const int t0 = ci * chunk;
+    if (bt.sx_on) {  // fused sharded step: global max over the ranks' pushed local maxima
+      for (int j = warp; j < G; j += 4) sx_global_max(bt, ws, b, h, j, lane);
+    } else if (threadIdx.x == 0) {
+      const int* gd = ws.group_done + b * bt.Hkv + h;
+      while (ld_acquire_gpu(gd) < 4 * s.nch) __nanosleep(256);
+    }
+    __syncthreads();
+    float gm[G], th[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const int row = b * bt.Hq + h * G + j;
+      gm[j] = bt.sx_on ? __ldcg(&ws.smaxbuf[row]) : dec_max(__ldcg(&ws.gmax[row]));
+      th[j] = gm[j] - bt.beta;
+    }
+    // this warp's quarter list
+    const int n = __ldcg(&ws.cnt[(size_t)c * 4 + warp]);
+    const int* gi = ws.gidx + (size_t)c * chunk + warp * qcap;
+    const float* gs = ws.cscore + (size_t)(c * 4 + warp) * G * qcap;
+    const T* vb = reinterpret_cast<const T*>(s.v) + (size_t)h * s.hs + (size_t)t0 * D + hl * DPL;
+    float acc[G][DPL], lsum[G];
+    int nsel[G], nret[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      lsum[j] = 0.f;
+      nsel[j] = nret[j] = 0;
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) acc[j][e] = 0.f;
+    }
+    // entries of the next batch are loaded while this batch is filtered and gathered
+    int row_n = lane < n ? __ldcg(gi + lane) : 0;
+    float sc_n[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) sc_n[j] = lane < n ? __ldcg(gs + j * qcap + lane) : -INFINITY;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      const int row = row_n;
+      float sc[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j) sc[j] = sc_n[j];
+      if (i0 + 32 < n) {
+        const int ii = i + 32;
+        row_n = ii < n ? __ldcg(gi + ii) : 0;
+#pragma unroll
+        for (int j = 0; j < G; ++j) sc_n[j] = ii < n ? __ldcg(gs + j * qcap + ii) : -INFINITY;
+      }
+      const bool valid = i < n;
+      const bool inwin = valid && in_window(s.off + t0 + row, s.P, bt.wi, bt.wl);
+      float w[G];
+      bool any = false;
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const bool pass = valid && sc[j] >= th[j];
+        const bool sel = pass && !inwin;
+        const unsigned bs = __ballot_sync(kFull, sel), br = __ballot_sync(kFull, pass);
+        if (sel)  // selected ids of (chunk, head j), quarter list `warp` (diagnostics)
+          ws.cidx[((size_t)c * G + j) * chunk + warp * qcap + nsel[j] + __popc(bs & lanemask_lt())] = row;
+        nsel[j] += __popc(bs);
+        nret[j] += __popc(br);
+        w[j] = sel ? exp2f((sc[j] - gm[j]) * k2) : 0.f;
+        lsum[j] += w[j];
+        any |= sel;
+      }
+      const unsigned ba = __ballot_sync(kFull, any);
+      const int na = __popc(ba);
+      if (any) {
+        const int pos = __popc(ba & lanemask_lt());
+        s_row[warp][pos] = row;
+#pragma unroll
+        for (int j = 0; j < G; ++j) s_w[warp][j][pos] = w[j];
+      }
+      __syncwarp();
+      for (int r0 = 0; r0 < na; r0 += 2 * U) {  // each kept row read once for all G heads
+        RawFrag<T, DPL> f[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int r = r0 + 2 * k + half;
+          if (r < na) f[k].load(vb + (size_t)s_row[warp][r] * D); else f[k].zero();
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int r = r0 + 2 * k + half;
+          float x[DPL];
+          f[k].to_float(x);
+#pragma unroll
+          for (int j = 0; j < G; ++j) {
+            const float wk = r < na ? s_w[warp][j][r] : 0.f;
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) acc[j][e] = fmaf(wk, x[e], acc[j][e]);
+          }
+        }
+      }
+      __syncwarp();
+    }
+    // the 4 quarter partials -> one (chunk, head) partial, summed in fixed order
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) acc[j][e] += __shfl_xor_sync(kFull, acc[j][e], 16);
+      const float l = warp_sum(lsum[j]);
+      if (lane == 0) { s_l[warp][j] = l; s_ns[warp][j] = nsel[j]; s_nr[warp][j] = nret[j]; }
+    }
+    const size_t cj0 = (size_t)c * G;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      if (warp > 0 && half == 0) {
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) s_red[warp - 1][hl * DPL + e] = acc[j][e];
+      }
+      __syncthreads();
+      if (warp == 0 && half == 0) {
+        float* pa = ws.part_acc + (cj0 + j) * D + hl * DPL;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e)
+          pa[e] = ((acc[j][e] + s_red[0][hl * DPL + e]) + s_red[1][hl * DPL + e]) + s_red[2][hl * DPL + e];
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x < G) {
+      const int j = threadIdx.x;
+      float l = 0.f;
+      int ns = 0, nr = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        l += s_l[q][j];
+        ns += s_ns[q][j];
+        nr += s_nr[q][j];
+        ws.ovl_sel[(cj0 + j) * 4 + q] = s_ns[q][j];
+        ws.ovl_ret[(cj0 + j) * 4 + q] = s_nr[q][j];
+      }
+      ws.part_l[cj0 + j] = l;
+      ws.selcnt[cj0 + j] = ns;
+      ws.retcnt[cj0 + j] = nr;
+    }
+  }
+  if (bt.trace && threadIdx.x == 0) trace_rec(bt, 2, 1);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Stage 3: one CTA per (sequence, query head): sum of the chunk partials (the
 // selected set, reference point = max; warps take interleaved chunks, fixed
@@ -659,7 +840,7 @@ __global__ void __launch_bounds__(CW * 32)
     for (int u = 0; u < U; ++u) {  // issue every load of the batch first
       const int cc = c + u * CW;
       const size_t cj = (size_t)(c0 + cc) * G + j;
-      tot[u] = cc < s.nch ? ws.heavy[cj] : 0;
+      tot[u] = (cc < s.nch && !bt.gfmt) ? ws.heavy[cj] : 0;  // group format: one partial per pair
       pl[u] = cc < s.nch ? ws.part_l[cj] : 0.f;
       ps[u] = cc < s.nch ? ws.selcnt[cj] : 0;
 #pragma unroll
@@ -789,6 +970,106 @@ __device__ __forceinline__ float to_f(T x) {
 // One CTA per (sequence, kv head).
 constexpr int kPrepSamples = 64;
 
+// Window partial of every q head of group (b, h) -- the base window ids this
+// shard holds + the session rows (reference store.py:274-282, window state of
+// attention.py:98-110): scores q.k / sqrt(d), (m, l, acc) per head, written to
+// ws.partbuf like the attend's window tasks. Computed in prep (it needs nothing
+// from the scan), so it is off the attend's tail. 8 warps take 4 rows per round
+// (K and V rows of a round in flight together), online softmax per warp, then a
+// fixed-order merge of the 8 warp states per head through shared memory.
+template <typename T, int D, int G>
+__device__ __forceinline__ void prep_window(const Batch& bt, const Ws& ws, const float (&qr)[G][(D + 31) / 32],
+                                            int b, int h, int64_t a0, int na, int64_t b0, int nbw, int lane,
+                                            int warp) {
+  constexpr int DL = (D + 31) / 32, RW = 4;
+  extern __shared__ float wsm[];  // [kWarps][G][D + 2]
+  const KSeq& s = bt.s[b];
+  const int R = na + nbw + seq_w(s);
+  const T* kbase = reinterpret_cast<const T*>(s.k) + (size_t)h * s.hs;
+  const T* vbase = reinterpret_cast<const T*>(s.v) + (size_t)h * s.hs;
+  const T* wkb = reinterpret_cast<const T*>(s.wk) + (size_t)h * s.whs;
+  const T* wvb = reinterpret_cast<const T*>(s.wv) + (size_t)h * s.whs;
+  float m[G], l[G], acc[G][DL];
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    m[j] = -INFINITY;
+    l[j] = 0.f;
+#pragma unroll
+    for (int k = 0; k < DL; ++k) acc[j][k] = 0.f;
+  }
+  for (int r0 = warp * RW; r0 < R; r0 += kWarps * RW) {
+    float kx[RW][DL], vx[RW][DL];
+#pragma unroll
+    for (int u = 0; u < RW; ++u) {
+      const int r = r0 + u;
+      const T *kr = nullptr, *vr = nullptr;
+      if (r < na) { kr = kbase + (size_t)(a0 + r) * D; vr = vbase + (size_t)(a0 + r) * D; }
+      else if (r < na + nbw) { kr = kbase + (size_t)(b0 + r - na) * D; vr = vbase + (size_t)(b0 + r - na) * D; }
+      else if (r < R) { kr = wkb + (size_t)(r - na - nbw) * D; vr = wvb + (size_t)(r - na - nbw) * D; }
+#pragma unroll
+      for (int k = 0; k < DL; ++k) {
+        const int e = lane + 32 * k;
+        kx[u][k] = (kr && e < D) ? to_f(kr[e]) : 0.f;
+        vx[u][k] = (vr && e < D) ? to_f(vr[e]) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      float z[RW], bm = -INFINITY;
+#pragma unroll
+      for (int u = 0; u < RW; ++u) {
+        float a = 0.f;
+#pragma unroll
+        for (int k = 0; k < DL; ++k) a = fmaf(qr[j][k], kx[u][k], a);
+        z[u] = r0 + u < R ? warp_sum(a) * bt.inv_sqrt_d : -INFINITY;
+        bm = fmaxf(bm, z[u]);
+      }
+      const float mn = fmaxf(m[j], bm);
+      const float sc = m[j] == -INFINITY ? 0.f : expf(m[j] - mn);
+      l[j] *= sc;
+#pragma unroll
+      for (int k = 0; k < DL; ++k) acc[j][k] *= sc;
+#pragma unroll
+      for (int u = 0; u < RW; ++u) {
+        const float w = r0 + u < R ? expf(z[u] - mn) : 0.f;
+        l[j] += w;
+#pragma unroll
+        for (int k = 0; k < DL; ++k) acc[j][k] = fmaf(w, vx[u][k], acc[j][k]);
+      }
+      m[j] = mn;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    float* o = wsm + ((size_t)warp * G + j) * (D + 2);
+    if (lane == 0) { o[0] = m[j]; o[1] = l[j]; }
+#pragma unroll
+    for (int k = 0; k < DL; ++k)
+      if (lane + 32 * k < D) o[2 + lane + 32 * k] = acc[j][k];
+  }
+  __syncthreads();
+  for (int j = warp; j < G; j += kWarps) {  // warp j merges head j's 8 warp states in order
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) M = fmaxf(M, wsm[((size_t)w * G + j) * (D + 2)]);
+    float f[kWarps], L = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const float mw = wsm[((size_t)w * G + j) * (D + 2)];
+      f[w] = (M == -INFINITY || mw == -INFINITY) ? 0.f : expf(mw - M);
+      L += wsm[((size_t)w * G + j) * (D + 2) + 1] * f[w];
+    }
+    float* pr = ws.partbuf + ((size_t)b * bt.Hq + h * G + j) * (D + 2);
+    if (lane == 0) { pr[0] = R > 0 ? M : -INFINITY; pr[1] = R > 0 ? L : 0.f; }
+    for (int e = lane; e < D; e += 32) {
+      float a = 0.f;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) a += wsm[((size_t)w * G + j) * (D + 2) + 2 + e] * f[w];
+      pr[2 + e] = R > 0 ? a : 0.f;
+    }
+  }
+}
+
 template <typename T, int D, int G>
 __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ Batch bt,
                                                         const float* __restrict__ q, Ws ws) {
@@ -845,7 +1126,7 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
       for (int i = threadIdx.x; i < rows; i += blockDim.x) ws.gmax[i] = 0u;
       for (int i = threadIdx.x; i < bt.B * bt.Hkv; i += blockDim.x) ws.group_done[i] = 0;
       if (threadIdx.x < 16) ws.counters[threadIdx.x] = 0;
-      if (threadIdx.x == 0) *ws.status = 0;
+      if (threadIdx.x == 0) { *ws.status = 0; *ws.mode = bt.gfmt; }
       __threadfence();
       __syncthreads();
       if (threadIdx.x == 0)
@@ -854,7 +1135,7 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
   } else {
     if (blockIdx.x == 0 && threadIdx.x < 16) {
       ws.counters[threadIdx.x] = 0;
-      if (threadIdx.x == 0) *ws.status = 0;
+      if (threadIdx.x == 0) { *ws.status = 0; *ws.mode = bt.gfmt; }
     }
     if (threadIdx.x == 0) ws.group_done[blockIdx.x] = 0;
   }
@@ -901,6 +1182,7 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
   if (lane == 0)
 #pragma unroll
     for (int j = 0; j < G; ++j) red[warp][j] = best[j];
+  if (bt.win_in_prep) prep_window<T, D, G>(bt, ws, qr, b, h, a0, na, b0, nbw, lane, warp);
   __syncthreads();
   if (async) {  // seeds join the running max once the header is zeroed
     __shared__ int s_ok;

@@ -79,16 +79,17 @@ __global__ void selected_kernel(const __grid_constant__ Batch bt, Ws ws, int64_t
   const KSeq& s = bt.s[b];
   const int c0 = s.chunk_base + h * s.nch;
   int base = 0, ret = 0;
+  const bool gfmt = *ws.mode != 0;  // group format (attend_grp_kernel): 4 quarter lists per pair
   for (int c = 0; c < s.nch; ++c) {
     const size_t cj = (size_t)(c0 + c) * bt.G + j;
-    const bool heavy = ws.heavy[cj] != 0;
+    const bool heavy = gfmt || ws.heavy[cj] != 0;
     for (int sq = 0; sq < (heavy ? 4 : 1); ++sq) {  // primary (in place from sub-list 0), overflow
-      const int n = sq == 0 ? ws.selcnt[cj] : ws.ovl_sel[cj * 4 + sq];
+      const int n = (sq == 0 && !gfmt) ? ws.selcnt[cj] : ws.ovl_sel[cj * 4 + sq];
       const int* src = ws.cidx + cj * bt.chunk + sq * (bt.chunk / 4);
       for (int i = threadIdx.x; i < n; i += blockDim.x)
         if (base + i < cap) ids[(size_t)row * cap + base + i] = s.off + (int64_t)c * bt.chunk + src[i];
       base += n;
-      ret += sq == 0 ? ws.retcnt[cj] : ws.ovl_ret[cj * 4 + sq];
+      ret += (sq == 0 && !gfmt) ? ws.retcnt[cj] : ws.ovl_ret[cj * 4 + sq];
     }
   }
   if (threadIdx.x == 0) { nsel[row] = base; nret[row] = ret; }

@@ -161,7 +161,7 @@ constexpr int kIds = 8;  // chunk-id ring (scheduler -> MMA warp + epilogue warp
 // rows of every 128-key tile). No cross-warp barriers: the warp keeps its own
 // running max (a max of real scores, hence a valid lower bound of the global
 // max) and writes its own ordered candidate sub-list (CandList, q = quarter).
-template <int G, int NP>
+template <int G, int NP, bool GF>
 __device__ __forceinline__ void epilogue_chunk(const Batch& bt, const Ws& ws, int c, int quarter,
                                                int lane, uint32_t tmem_base, uint32_t accf0,
                                                uint32_t acce0, int& acc, uint32_t& aphase,
@@ -187,11 +187,6 @@ __device__ __forceinline__ void epilogue_chunk(const Batch& bt, const Ws& ws, in
   const int qoff = quarter * (chunk / 4);
   for (unsigned long long m = chunk_tiles(bt, ws, c, ntiles); m; m &= m - 1) {
     const int tl = __ffsll((long long)m) - 1;
-    if (bt.trace && quarter == 0) {  // diagnostics: epilogue time waiting for MMA results (slot 12, ns)
-      const unsigned long long t0 = gtimer();
-      mbar_wait(accf0 + 8u * acc, (aphase >> acc) & 1u);
-      if (lane == 0) trace_add(bt, 1, 12, gtimer() - t0);
-    }
     mbar_wait(accf0 + 8u * acc, (aphase >> acc) & 1u);
     fence_after();
     float v[NP];
@@ -221,9 +216,27 @@ __device__ __forceinline__ void epilogue_chunk(const Batch& bt, const Ws& ws, in
       for (int j = 0; j < G; ++j) run[j] = dec_max(pre[j]);
     }
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
+    for (int j = 0; j < G; ++j)
 #pragma unroll
       for (int qq = 0; qq < 4; ++qq) run[j] = fmaxf(run[j], tmax[(tb * 4 + qq) * G + j]);
+    if constexpr (GF) {  // one entry per row some head keeps: the row and all G scores
+      bool pass = false;
+#pragma unroll
+      for (int j = 0; j < G; ++j) pass |= sc[j] >= run[j] - bt.beta;
+      pass = pass && ok;
+      const unsigned bal = __ballot_sync(kFull, pass);
+      if (pass) {
+        const int o = cnt[0] + __popc(bal & lanemask_lt());
+        ws.gidx[(size_t)c * chunk + qoff + o] = row;
+        float* gsc = ws.cscore + (size_t)(c * 4 + quarter) * G * (chunk / 4) + o;
+#pragma unroll
+        for (int j = 0; j < G; ++j) gsc[j * (chunk / 4)] = sc[j];
+      }
+      cnt[0] += __popc(bal);
+      continue;
+    }
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
       const bool pass = ok && sc[j] >= (bt.topk_thr ? tk[j] : run[j] - bt.beta);
       const unsigned bal = __ballot_sync(kFull, pass);
       if (pass) {
@@ -233,6 +246,15 @@ __device__ __forceinline__ void epilogue_chunk(const Batch& bt, const Ws& ws, in
       }
       cnt[j] += __popc(bal);
     }
+  }
+  if constexpr (GF) {
+    if (lane == 0) ws.cnt[(size_t)c * 4 + quarter] = cnt[0];
+    if (quarter == 0 && lane < G) {
+#pragma unroll
+      for (int j = 0; j < G; ++j)
+        if (j == lane && enc_max(run[j]) > pre[j]) atomicMax(&ws.gmax[b * bt.Hq + h * G + j], enc_max(run[j]));
+    }
+    return;
   }
   if (lane < G) {
 #pragma unroll
@@ -285,7 +307,7 @@ constexpr int scan_tc_maxreg() {
   return kStages <= 2 ? (3 * G <= 16 ? ALAYA_SCAN_MAXREG_S2 : 80) : (kStages <= 3 ? ALAYA_SCAN_MAXREG_S3 : 168);
 }
 
-template <int G, int kStages>
+template <int G, int kStages, bool GF>
 __global__ void __launch_bounds__(kThreadsTc) __maxnreg__((scan_tc_maxreg<G, kStages>()))
     scan_tc_kernel(const __grid_constant__ Batch bt, const __grid_constant__ Maps maps,
                    const float* __restrict__ q, Ws ws) {
@@ -455,11 +477,6 @@ __global__ void __launch_bounds__(kThreadsTc) __maxnreg__((scan_tc_maxreg<G, kSt
       uint8_t* bb = b_buf + bi * kBBytes;
       bool first = true;
       for (unsigned long long m = chunk_tiles(bt, ws, c, ntiles); m; m &= m - 1) {
-        if (bt.trace) {  // diagnostics: MMA warp waiting for a free accumulator (slot 10, ns)
-          const unsigned long long t0 = gtimer();
-          mbar_wait(acce0 + 8u * acc, ((ephase >> acc) & 1u) ^ 1u);
-          if (lane == 0) trace_add(bt, 1, 10, gtimer() - t0);
-        }
         mbar_wait(acce0 + 8u * acc, ((ephase >> acc) & 1u) ^ 1u);
         ephase ^= 1u << acc;
         fence_after();
@@ -472,11 +489,6 @@ __global__ void __launch_bounds__(kThreadsTc) __maxnreg__((scan_tc_maxreg<G, kSt
           build_b_smem<G, NP>(bb, q_stage, lane);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-        }
-        if (bt.trace) {  // diagnostics: MMA warp waiting for TMA data (slot 11, ns)
-          const unsigned long long t0 = gtimer();
-          mbar_wait(full_bar(stage), phase);
-          if (lane == 0) trace_add(bt, 1, 11, gtimer() - t0);
         }
         mbar_wait(full_bar(stage), phase);
         fence_after();
@@ -559,8 +571,8 @@ __global__ void __launch_bounds__(kThreadsTc) __maxnreg__((scan_tc_maxreg<G, kSt
     if (c >= 0) load_pre(c);
     for (int k = 0; c >= 0; ++k) {
       int b, h;
-      epilogue_chunk<G, NP>(bt, ws, c, quarter, lane, tmem_base, accf0, acce0, acc, aphase, b, h,
-                            tmax, tcount, pre);
+      epilogue_chunk<G, NP, GF>(bt, ws, c, quarter, lane, tmem_base, accf0, acce0, acc, aphase, b, h,
+                                tmax, tcount, pre);
       const int nxt = read_id(k + 1);  // posted by now (the producer is >= 2 tiles ahead)
       if (quarter == 0 && lane == 0 && k < 8) trace_rec(bt, 1, 2 + k);
       const unsigned long long t_pub = bt.trace ? gtimer() : 0ull;

@@ -50,10 +50,23 @@ template <int G, int S>
 int launch_s(const Batch& bt, const tc::Maps& maps, const float* q, const Ws& ws, cudaStream_t st,
              int ctas_per_sm) {
   const size_t sm = tc::tc_smem_bytes(G, S);
-  cudaFuncSetAttribute(tc::scan_tc_kernel<G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   // persistent: every resident slot, chunks handed out dynamically (scan_tc_kernel)
   const int grid = std::min(bt.total_chunks, ctas_per_sm * num_sms());
-  return launch_pdl("scan_tc_kernel", tc::scan_tc_kernel<G, S>, grid, tc::kThreadsTc, sm, st, bt, maps, q, ws);
+  if (bt.gfmt) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(tc::scan_tc_kernel<G, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      attr = true;
+    }
+    return launch_pdl("scan_tc_kernel", tc::scan_tc_kernel<G, S, true>, grid, tc::kThreadsTc, sm, st, bt, maps, q,
+                      ws);
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tc::scan_tc_kernel<G, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  return launch_pdl("scan_tc_kernel", tc::scan_tc_kernel<G, S, false>, grid, tc::kThreadsTc, sm, st, bt, maps, q, ws);
 }
 
 // Persistent CTAs per SM (ALAYA_TC_CTAS, default 3): 2 CTAs with 3-stage rings
@@ -122,6 +135,18 @@ bool pdl_enabled() {
 // attend beside the scan: on for every tcgen05 call (ALAYA_OVERLAP=0 turns it
 // off). On since the async prep / combine changes (v16): B=1 89.0 -> 86.1 us,
 // B=2 132.7 -> 129.0, 8K ctx B=4 55.9 -> 51.6 (tools/probe_latency.py)
+// Group candidate format + attend_grp_kernel (V rows gathered once per GQA
+// group): ALAYA_GFMT=1 on, 0 off, default (-1) on when beta / sqrt(d) >= 11.5
+// (beta >= 130 at d = 128). It pays G FMAs per gathered row, so it only wins
+// when the heads of a group keep mostly the same rows; on the reference
+// generator's data that is the high-beta regime (B=4 128K: beta 140 602 -> 445
+// us, beta 110 226 -> 259 us; profiles/r02/README.md).
+bool gfmt_enabled(const Batch& bt) {
+  static const int mode = env_int("ALAYA_GFMT", -1);
+  if (mode >= 0) return mode != 0;
+  return bt.beta * bt.inv_sqrt_d >= 11.5f;
+}
+
 bool overlap_enabled() {
   static const int mode = env_int("ALAYA_OVERLAP", 1);
   return mode != 0;

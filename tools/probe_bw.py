@@ -41,6 +41,12 @@ for mode, name in [(0, "ldg_stream"), (1, "bulk_tma_stream"), (3, "tma2d_two_box
                    (4, "tma3d_one_box_stream")]:
     t = timeit(lambda: lib.alaya_diag_read(buf.data_ptr(), nbytes, mode, None, 0, sink.data_ptr(), st))
     out[name + "_GBps"] = round(nbytes / t / 1e9, 1)
+# size dependence: one launch over the first S bytes (fixed per-launch ramp/drain cost)
+for size in (268435456, 536870912, 1073741824, 2147483648):
+    for mode, name in [(0, "ldg"), (1, "bulk"), (3, "tma2d")]:
+        t = timeit(lambda: lib.alaya_diag_read(buf.data_ptr(), size, mode, None, 0, sink.data_ptr(), st), reps=20)
+        out[f"{name}_{size >> 20}MB_us"] = round(t * 1e6, 1)
+        out[f"{name}_{size >> 20}MB_GBps"] = round(size / t / 1e9, 1)
 # V-gather pattern: 24% of 256-byte rows, random positions, ascending
 rows_total = nbytes // 256
 g = torch.Generator(device=dev).manual_seed(0)

@@ -30,6 +30,7 @@ ap.add_argument("--beta", type=float, default=110.0)
 ap.add_argument("--label", default="base")
 ap.add_argument("--out", default=None)
 ap.add_argument("--isolated", action="store_true", help="trace one call on an idle GPU")
+ap.add_argument("--scan-only", action="store_true", help="prep + scan only (alaya_scan, no attend)")
 a = ap.parse_args()
 dev = torch.device("cuda")
 lib = _lib.load()
@@ -71,15 +72,16 @@ for B in [int(x) for x in a.batches.split(",")]:
     pick = torch.randint(0, 16, (B, a.hq), generator=g, device=dev)
     q = (centers[pick] + 0.25 * torch.randn(B, a.hq, d, generator=g, device=dev)).float()
     out = torch.empty_like(q)
-    t_call = timed(lambda: call.dipr_attention(q, out=out))
+    fn = (lambda: call.scan_only(q)) if a.scan_only else (lambda: call.dipr_attention(q, out=out))
+    t_call = timed(fn)
     buf = torch.zeros(4 * NCTA * NSLOT, dtype=torch.int64, device=dev)
     _lib.check(lib.alaya_debug_trace(ctypes.c_void_p(buf.data_ptr()), buf.numel() * 8))
     try:
-        call.dipr_attention(q, out=out)
+        fn()
         if a.isolated:
             torch.cuda.synchronize()
             buf.zero_()
-        call.dipr_attention(q, out=out)
+        fn()
         torch.cuda.synchronize()
     finally:
         _lib.check(lib.alaya_debug_trace(None, 0))
@@ -88,7 +90,7 @@ for B in [int(x) for x in a.batches.split(",")]:
               if x > 0 and not (ki == 2 and si in (4, 5)) and not (ki == 1 and si >= 10)]  # sums
     t0 = min(stamps)
     us = lambda x: round((x - t0) / 1e3, 2)  # noqa: E731
-    line = {"label": a.label + ("/isolated" if a.isolated else ""), "B": B, "ctx": a.ctx, "chunk": a.chunk, "us_call_timed": round(t_call, 1)}
+    line = {"label": a.label + ("/isolated" if a.isolated else "") + ("/scan" if a.scan_only else ""), "B": B, "ctx": a.ctx, "chunk": a.chunk, "us_call_timed": round(t_call, 1)}
     for ki, name in enumerate(KINDS):
         ctas = [cta for cta in tr[ki] if cta[0] > 0]
         if not ctas:
@@ -99,11 +101,11 @@ for B in [int(x) for x in a.batches.split(",")]:
                       "end_p10": pct(ends, 0.1), "end_p50": pct(ends, 0.5), "end_p90": pct(ends, 0.9),
                       "end_max": max(ends) if ends else None}
         if name == "scan":  # chunk-completion times of each round (slot 2 + round)
-            for si, key in ((10, "mma_wait_acc"), (11, "mma_wait_data"), (12, "epi_wait_mma"),
-                            (13, "producer_wait_ring"), (14, "epi_publish"), (15, "producer_publish")):
+            for si, key in ((13, "producer_wait_ring"), (14, "epi_publish"), (15, "publisher")):
                 v = [x[si] / 1e3 for x in ctas]
                 line[name][key + "_us_mean"] = round(sum(v) / len(v), 2)
             rounds = []
+            line[name]["end_hist_us"] = [sum(1 for x in ends if lo <= x < lo + 5) for lo in range(0, 400, 5)]
             for r in range(8):
                 e = [us(x[2 + r]) for x in ctas if x[2 + r] > 0]
                 if not e:
