@@ -1,5 +1,6 @@
 // C-ABI entry points (include/alaya.h): validation, workspace layout, kernel
 // dispatch over (dtype, dim, group size) and launch.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -489,8 +490,19 @@ int alaya_selected(const alaya_params* p, const alaya_seq* seqs, int batch, int6
   int rc = prepare(p, seqs, batch, d_ws, ws_bytes, stream, &c);
   if (rc) return rc;
   if (!d_ids || !d_selected || !d_retrieved) return fail(ALAYA_ERR_ARG, "null outputs");
-  selected_kernel<<<batch * c.bt.Hq, kThreads, 0, c.stream>>>(c.bt, c.ws, d_ids, cap, d_selected,
-                                                              d_retrieved);  // (format: ws.mode)
+  int max_nch = 0;
+  for (int b = 0; b < batch; ++b) max_nch = std::max(max_nch, c.bt.s[b].nch);
+  const size_t sm = 4 * ((size_t)max_nch + 1);  // chunk offsets
+  if (sm > 48 * 1024) {
+    static size_t attr = 0;
+    if (sm > attr) {
+      cudaFuncSetAttribute(selected_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      attr = sm;
+    }
+  }
+  const dim3 grid(batch * c.bt.Hq, std::max(1, (max_nch + kWarps - 1) / kWarps));  // a warp per chunk
+  selected_kernel<<<grid, kThreads, sm, c.stream>>>(c.bt, c.ws, d_ids, cap, d_selected,
+                                                    d_retrieved);  // (format: ws.mode)
   return cuda_check("selected_kernel");
 }
 

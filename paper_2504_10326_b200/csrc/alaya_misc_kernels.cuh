@@ -71,28 +71,107 @@ __global__ void window_commit_kernel(const __grid_constant__ Batch bt) {
 }
 
 // Selected ids (global, ascending) + counts per (sequence, q head).
-__global__ void selected_kernel(const __grid_constant__ Batch bt, Ws ws, int64_t* __restrict__ ids,
-                                int64_t cap, int32_t* __restrict__ nsel, int32_t* __restrict__ nret) {
-  const int row = blockIdx.x;  // b*Hq + qh
+__global__ void __launch_bounds__(kThreads) selected_kernel(const __grid_constant__ Batch bt, Ws ws,
+                                                          int64_t* __restrict__ ids, int64_t cap,
+                                                          int32_t* __restrict__ nsel, int32_t* __restrict__ nret) {
+  // Grid (rows, splits): CTA (row = seq*Hq + q head, split) writes the selected ids
+  // of chunks [split*8, split*8 + 8) of the row in ASCENDING order (the
+  // reference's sorted diagnostics, store.py:288-292), one chunk per warp, at
+  // the chunk's offset in the row (a block scan of the per-chunk counts), and
+  // only up to the row's selected count. A chunk's selection sits in up to 4
+  // ordered sub-lists (lane quarters of the tcgen05 scan, split pairs,
+  // group-format quarters) whose rows interleave; the warp ORs them into a
+  // chunk-row bitmap in shared memory and emits the set bits in order.
+  constexpr int kMaxWords = 8192 / 32;  // chunk <= 8192
+  __shared__ unsigned bm[kWarps][kMaxWords];
+  __shared__ int wsum[kWarps], wret[kWarps];
+  extern __shared__ int chunk_base[];   // [nch] exclusive prefix of selected counts
+  const int row = blockIdx.x;
   const int b = row / bt.Hq, qh = row - b * bt.Hq;
   const int h = qh / bt.G, j = qh - h * bt.G;
   const KSeq& s = bt.s[b];
   const int c0 = s.chunk_base + h * s.nch;
-  int base = 0, ret = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool gfmt = *ws.mode != 0;  // group format (attend_grp_kernel): 4 quarter lists per pair
-  for (int c = 0; c < s.nch; ++c) {
+  auto nlists = [&](size_t cj) { return (gfmt || ws.heavy[cj] != 0) ? 4 : 1; };
+  auto count_of = [&](size_t cj, int sq) {
+    return (sq == 0 && !gfmt) ? ws.selcnt[cj] : ws.ovl_sel[cj * 4 + sq];
+  };
+  // per-chunk counts: thread t owns the contiguous chunks [t*seg, (t+1)*seg)
+  const int seg = (s.nch + blockDim.x - 1) / blockDim.x;
+  const int cb = threadIdx.x * seg, ce = min(s.nch, cb + seg);
+  int mine = 0, mret = 0;
+  for (int c = cb; c < ce; ++c) {
     const size_t cj = (size_t)(c0 + c) * bt.G + j;
-    const bool heavy = gfmt || ws.heavy[cj] != 0;
-    for (int sq = 0; sq < (heavy ? 4 : 1); ++sq) {  // primary (in place from sub-list 0), overflow
-      const int n = (sq == 0 && !gfmt) ? ws.selcnt[cj] : ws.ovl_sel[cj * 4 + sq];
-      const int* src = ws.cidx + cj * bt.chunk + sq * (bt.chunk / 4);
-      for (int i = threadIdx.x; i < n; i += blockDim.x)
-        if (base + i < cap) ids[(size_t)row * cap + base + i] = s.off + (int64_t)c * bt.chunk + src[i];
-      base += n;
-      ret += (sq == 0 && !gfmt) ? ws.retcnt[cj] : ws.ovl_ret[cj * 4 + sq];
+    int n = 0;
+    for (int sq = 0, L = nlists(cj); sq < L; ++sq) {
+      n += count_of(cj, sq);
+      mret += (sq == 0 && !gfmt) ? ws.retcnt[cj] : ws.ovl_ret[cj * 4 + sq];
+    }
+    chunk_base[c] = n;
+    mine += n;
+  }
+  // block exclusive scan of the per-thread sums
+  int incl = mine;
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) {
+    const int y = __shfl_up_sync(kFull, incl, m);
+    if (lane >= m) incl += y;
+  }
+  int r = mret;
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) r += __shfl_xor_sync(kFull, r, m);
+  if (lane == 31) wsum[warp] = incl;
+  if (lane == 0) wret[warp] = r;
+  __syncthreads();
+  int before = 0, total = 0, rtot = 0;
+  for (int w = 0; w < kWarps; ++w) {
+    if (w < warp) before += wsum[w];
+    total += wsum[w];
+    rtot += wret[w];
+  }
+  int run = before + incl - mine;
+  for (int c = cb; c < ce; ++c) {
+    const int n = chunk_base[c];
+    chunk_base[c] = run;
+    run += n;
+  }
+  if (blockIdx.y == 0 && threadIdx.x == 0) { nsel[row] = total; nret[row] = rtot; }
+  __syncthreads();
+  const int words = (bt.chunk + 31) / 32;
+  unsigned* bw = bm[warp];
+  const int c = blockIdx.y * kWarps + warp;
+  if (c >= s.nch) return;
+  const size_t cj = (size_t)(c0 + c) * bt.G + j;
+  for (int w = lane; w < words; w += 32) bw[w] = 0u;
+  __syncwarp();
+  for (int sq = 0, L = nlists(cj); sq < L; ++sq) {
+    const int n = count_of(cj, sq);
+    const int* src = ws.cidx + cj * bt.chunk + sq * (bt.chunk / 4);
+    for (int i = lane; i < n; i += 32) {
+      const int rr = src[i];
+      atomicOr(&bw[rr >> 5], 1u << (rr & 31));
     }
   }
-  if (threadIdx.x == 0) { nsel[row] = base; nret[row] = ret; }
+  __syncwarp();
+  int out = chunk_base[c];
+  for (int w0 = 0; w0 < words; w0 += 32) {
+    const int w = w0 + lane;
+    const unsigned bits = w < words ? bw[w] : 0u;
+    const int cnt = __popc(bits);
+    int in = cnt;
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1) {
+      const int y = __shfl_up_sync(kFull, in, m);
+      if (lane >= m) in += y;
+    }
+    int pos = out + in - cnt;
+    for (unsigned x = bits; x; x &= x - 1) {
+      if (pos < cap) ids[(size_t)row * cap + pos] = s.off + (int64_t)c * bt.chunk + w * 32 + (__ffs(x) - 1);
+      ++pos;
+    }
+    out += __shfl_sync(kFull, in, 31);
+  }
 }
 
 // Session-window append: one thread per element of [B][Hkv][D].

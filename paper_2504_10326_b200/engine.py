@@ -396,12 +396,8 @@ class Call:
         check(self.lib.alaya_selected(ctypes.byref(self.params), self.seqs, self.B, ids.data_ptr(),
                                       ids.shape[1], nsel.data_ptr(), nret.data_ptr(),
                                       self.ws.data_ptr(), self.ws_bytes, self.stream))
-        # the tcgen05 scan emits per-lane-quarter sub-lists: sort each row (reference
-        # diagnostics are sorted, store.py:289); padding sorts to the end
-        col = torch.arange(ids.shape[1], device=self.device)
-        ids = torch.where(col[None, :] < nsel[:, None].long(), ids,
-                          torch.full_like(ids, torch.iinfo(torch.int64).max))
-        ids = torch.sort(ids, dim=1).values
+        # rows come back ascending from the kernel (the reference's diagnostics are
+        # sorted, store.py:289); only the first nsel[row] entries of a row are written
         return ids, nsel, nret
 
 

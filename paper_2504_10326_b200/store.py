@@ -324,7 +324,9 @@ class Session:
                               "query_head": qh})
             return {"layer": layer, "plan": active, "heads": heads}
         layer, active, ids, nsel, nret, p, wi, wl = self._diag
-        ids, nsel, nret = ids.cpu().numpy(), nsel.cpu().numpy(), nret.cpu().numpy()
+        nsel, nret = nsel.cpu().numpy(), nret.cpu().numpy()
+        width = int(nsel.max()) if nsel.size else 0  # rows are written up to their count only
+        ids = ids[:, :max(width, 1)].cpu().numpy()
         window = WindowConfig(wi, wl).base_ids(p).tolist()
         heads = []
         for qh in range(ids.shape[0]):

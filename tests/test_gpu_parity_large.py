@@ -56,7 +56,7 @@ def _round_bf16(x: np.ndarray, dev) -> tuple[torch.Tensor, np.ndarray]:
     return t, t.float().cpu().numpy()
 
 
-def _check_session(out_b, diag, q_b, keys, vals, wk, wv, hq, kv, stats):
+def _check_session(out_b, diag, q_b, keys, vals, wk, wv, hq, kv, stats, beta=BETA):
     """All heads of one session: epsilon set rule, retrieved count, outputs."""
     g = hq // HKV
     eps = EPS_SET[kv]
@@ -68,8 +68,8 @@ def _check_session(out_b, diag, q_b, keys, vals, wk, wv, hq, kv, stats):
             qh = h * g + j
             info = diag["heads"][qh]
             got = np.asarray(info["selected_base"], np.int64)
-            flips, margin = set_flips(got, S[:, j], BETA, eps, window)
-            assert retrieved_ok(info["retrieved"], S[:, j], BETA, eps), (qh, info["retrieved"])
+            flips, margin = set_flips(got, S[:, j], beta, eps, window)
+            assert retrieved_ok(info["retrieved"], S[:, j], beta, eps), (qh, info["retrieved"])
             o_sel = O.head_attention_on_selection(q_b[qh], keys[h], vals[h], wk[h], wv[h], got)
             e = rel(out_b[qh], o_sel)
             assert e <= 1e-5, (qh, e)
@@ -82,11 +82,11 @@ def _check_session(out_b, diag, q_b, keys, vals, wk, wv, hq, kv, stats):
             stats["selected"] += got.size
 
 
-def _run_sessions(ctxs, hq, kv, scan, n_sessions, seed):
+def _run_sessions(ctxs, hq, kv, scan, n_sessions, seed, beta=BETA):
     import paper_2504_10326_b200 as P
     dev = torch.device("cuda")
     shape = P.ModelShape(1, hq, HKV, D)
-    cfg = P.EngineConfig(beta=BETA, first_layers=(0,), short_context_threshold=0, kv_dtype=kv,
+    cfg = P.EngineConfig(beta=beta, first_layers=(0,), short_context_threshold=0, kv_dtype=kv,
                          scan_kernel=scan)
     db = P.ContextStore(shape, cfg)
     host = {}
@@ -122,8 +122,8 @@ def _run_sessions(ctxs, hq, kv, scan, n_sessions, seed):
         w = s._wlen[0]
         wk = s._wk[0, :, :w].float().cpu().numpy()
         wv = s._wv[0, :, :w].float().cpu().numpy()
-        _check_session(out[b], s.last_diagnostics, q[b], keys, vals, wk, wv, hq, kv, stats)
-    print(f"{hq}q/{HKV}kv {kv} {scan} B={n_sessions}: {stats}")
+        _check_session(out[b], s.last_diagnostics, q[b], keys, vals, wk, wv, hq, kv, stats, beta)
+    print(f"{hq}q/{HKV}kv {kv} {scan} B={n_sessions} beta={beta:g}: {stats}")
     assert stats["heads"] == n_sessions * hq
     # the epsilon band is thin at 128K: flips stay rare (<= 1 per head)
     assert stats["flips"] <= stats["heads"]
@@ -141,6 +141,14 @@ def test_llama_128k_fp32_cuda_core_b4(cuda_ok, ctx128):
 @pytest.mark.parametrize("scan,batch", [("tcgen05", 1), ("tcgen05", 8), ("cuda_core", 1)])
 def test_qwen_128k_bf16(cuda_ok, ctx128, scan, batch):
     _run_sessions(ctx128, 40, "bfloat16", scan, batch, seed=300 + batch)
+
+
+@pytest.mark.parametrize("hq,batch", [(32, 2), (40, 1)])
+def test_128k_bf16_high_beta_group_format(cuda_ok, ctx128, hq, batch):
+    """beta = 140 (beta / sqrt(d) >= 11.5): the tcgen05 scan writes the group
+    candidate format and attend_grp_kernel gathers each V row once per GQA group
+    (about 60 % of the tokens selected per head here); same rules, every head."""
+    _run_sessions(ctx128, hq, "bfloat16", "tcgen05", batch, seed=400 + hq, beta=140.0)
 
 
 # ---------------------------------------------------------------------------
