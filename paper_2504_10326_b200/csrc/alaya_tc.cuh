@@ -233,18 +233,18 @@ __device__ __forceinline__ void epilogue_chunk(const Batch& bt, const Ws& ws, in
         for (int j = 0; j < G; ++j) gsc[j * (chunk / 4)] = sc[j];
       }
       cnt[0] += __popc(bal);
-      continue;
-    }
+    } else {
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      const bool pass = ok && sc[j] >= (bt.topk_thr ? tk[j] : run[j] - bt.beta);
-      const unsigned bal = __ballot_sync(kFull, pass);
-      if (pass) {
-        const int o = qoff + cnt[j] + __popc(bal & lanemask_lt());
-        ws.cidx[(cbase + j) * chunk + o] = row;
-        ws.cscore[(cbase + j) * chunk + o] = sc[j];
+      for (int j = 0; j < G; ++j) {
+        const bool pass = ok && sc[j] >= (bt.topk_thr ? tk[j] : run[j] - bt.beta);
+        const unsigned bal = __ballot_sync(kFull, pass);
+        if (pass) {
+          const int o = qoff + cnt[j] + __popc(bal & lanemask_lt());
+          ws.cidx[(cbase + j) * chunk + o] = row;
+          ws.cscore[(cbase + j) * chunk + o] = sc[j];
+        }
+        cnt[j] += __popc(bal);
       }
-      cnt[j] += __popc(bal);
     }
   }
   if constexpr (GF) {
