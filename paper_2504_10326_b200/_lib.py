@@ -126,8 +126,9 @@ def load() -> ctypes.CDLL:
     lib.alaya_last_error.restype = ctypes.c_char_p
     lib.alaya_last_error.argtypes = []
     lib.alaya_version.restype = i32
-    lib.alaya_debug_trace.restype = i32
-    lib.alaya_debug_trace.argtypes = [vp, ctypes.c_int64]
+    if hasattr(lib, "alaya_debug_trace"):  # (absent from older diagnostic build variants)
+        lib.alaya_debug_trace.restype = i32
+        lib.alaya_debug_trace.argtypes = [vp, ctypes.c_int64]
     lib.alaya_workspace_bytes.restype = sz
     lib.alaya_workspace_bytes.argtypes = [P, S, i32]
     lib.alaya_dipr_attention.restype = i32

@@ -50,8 +50,15 @@ template <int G, int S>
 int launch_s(const Batch& bt, const tc::Maps& maps, const float* q, const Ws& ws, cudaStream_t st,
              int ctas_per_sm) {
   const size_t sm = tc::tc_smem_bytes(G, S);
-  // persistent: every resident slot, chunks handed out dynamically (scan_tc_kernel)
-  const int grid = std::min(bt.total_chunks, ctas_per_sm * num_sms());
+  // persistent, chunks handed out dynamically; `less` SMs run one scan CTA instead
+  // of two so attend CTAs fit beside it (an attend CTA cannot share an SM with two
+  // scan CTAs: registers), more of them as the attend work grows with the number of
+  // (sequence, kv head) groups (measured at 128K, profiles/r02/grid_less_v29.jsonl:
+  // B=1 best at 24-48, B=4 at 48-74, B=8 at 110). ALAYA_TC_GRID_LESS overrides.
+  static const int less_env = env_int("ALAYA_TC_GRID_LESS", -1);
+  const int groups = bt.B * bt.Hkv;
+  const int less = less_env >= 0 ? less_env : std::min(110, 24 + 3 * groups / 2);
+  const int grid = std::min(bt.total_chunks, std::max(num_sms(), ctas_per_sm * num_sms() - less));
   if (bt.gfmt) {
     static bool attr = false;
     if (!attr) {
