@@ -369,15 +369,17 @@ def main():
     def step(s):
         w = a.window_rows + s + 1
         for l in range(L):
+            if world == 1:  # Session.update + Session.attention in one call (the append
+                calls[l].set_window_rows(w)  # runs in the call's first kernel)
+                calls[l].dipr_attention(Q[s, l], out=out[l], append=(KNf[s, l], VNf[s, l]))
+                continue
             if kv_ring_owner or a.check:  # Session.update: append this token's K/V
                 for sv in append_seqs[l]:   # (--check: every rank mirrors the ring so
                     sv.w = w - 1            # rank 0 can run the unsharded reference)
                 engine.window_append(append_seqs[l], append_params, dtype, KNf[s, l], VNf[s, l])
             if kv_ring_owner:
                 calls[l].set_window_rows(w)
-            if world == 1:
-                calls[l].dipr_attention(Q[s, l], out=out[l])
-            else:  # scan -> max-allreduce -> attend -> allgather -> merge
+            if True:  # scan -> max-allreduce -> attend -> allgather -> merge
                 out[l].copy_(sharded_attention(stages[l], Q[s, l], exchange=exch))
 
     for s in range(a.warmup):
@@ -527,11 +529,12 @@ def main():
                            "parallelism": "seq-shard%d" % world if world > 1 else "single",
                            "collectives": collective},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                # per layer: window append + (single GPU) prep, scan, attend, combine, or
+                # per layer: (single GPU) prep (with the window append), scan, attend,
+                # combine, or window append +
                 # (sharded) prep, scan, combine (local max), attend, combine (partial), merge
                 # + 2 exchanges (peer path; NCCL's own kernels not counted), or (fused
                 # peer path) prep, scan, attend, combine (pushes to peers), merge
-                "gpu_launches": a.steps * L * (5 if world == 1 else
+                "gpu_launches": a.steps * L * (4 if world == 1 else
                                                {"p2p": 9, "p2p-fused": 6}.get(collective, 7)),
                 "clocks": sampler.summary(), "parity": parity, "stats": stats,
                 "sharded_check": sharded_check,

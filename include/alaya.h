@@ -9,6 +9,7 @@
  *   alaya_dipr_attention   Session.attention on the DIPR/FLAT plan
  *                          (store.py:191-216 -> _head_attention :252-293,
  *                          _retrieve flat branch :336-337).
+ *   alaya_dipr_attention_update  Session.update (store.py:160-189) + the above.
  *   alaya_scan             inner_products + scores.max()  (core.py:64-67,
  *                          dipr.py:63-64), batched over GQA groups.
  *   alaya_attend           mask s >= max - beta (dipr.py:64), setdiff with the
@@ -141,6 +142,17 @@ size_t alaya_workspace_bytes(const alaya_params* p, const alaya_seq* seqs, int b
 int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch,
                          const float* d_q, float* d_out, void* d_ws, size_t ws_bytes,
                          void* stream);
+
+/* Session.update followed by Session.attention for one layer of a batch
+ * (store.py:160-189 then 191-216) in one call: the new K/V row of every
+ * sequence (d_k_new/d_v_new [batch][Hkv][dim] fp32, rounded to the KV dtype)
+ * is written as window row seqs[b].w - 1 -- seqs[b].w counts the windows rows
+ * INCLUDING the new one -- by the call's first kernel, then the same step as
+ * alaya_dipr_attention. Saves the separate alaya_window_append launch.
+ * Not for device window counts (d_w). */
+int alaya_dipr_attention_update(const alaya_params* p, const alaya_seq* seqs, int batch,
+                                const float* d_k_new, const float* d_v_new, const float* d_q,
+                                float* d_out, void* d_ws, size_t ws_bytes, void* stream);
 
 /* Stage 1: score every base key of every query head, per-head max and the
  * candidate superset. Writes the local max per (seq, q head) to d_smax

@@ -36,6 +36,7 @@ MAX_BATCH = 128
 # every symbol include/alaya.h declares (checked by tests/test_boundary.py)
 EXPORTS = (
     "alaya_last_error", "alaya_version", "alaya_workspace_bytes", "alaya_dipr_attention",
+    "alaya_dipr_attention_update",
     "alaya_scan", "alaya_attend", "alaya_sharded_step", "alaya_merge_exchanged", "alaya_merge_partials", "alaya_merge_states", "alaya_selected",
     "alaya_ws_status", "alaya_window_append", "alaya_block_bounds", "alaya_ws_block_stats",
     "alaya_ws_candidate_counts", "alaya_topk", "alaya_block_reps", "alaya_block_topk",
@@ -133,6 +134,8 @@ def load() -> ctypes.CDLL:
     lib.alaya_workspace_bytes.argtypes = [P, S, i32]
     lib.alaya_dipr_attention.restype = i32
     lib.alaya_dipr_attention.argtypes = [P, S, i32, vp, vp, vp, sz, vp]
+    lib.alaya_dipr_attention_update.restype = i32
+    lib.alaya_dipr_attention_update.argtypes = [P, S, i32, vp, vp, vp, vp, vp, sz, vp]
     lib.alaya_scan.restype = i32
     lib.alaya_scan.argtypes = [P, S, i32, vp, vp, vp, sz, vp]
     lib.alaya_sharded_step.restype = i32

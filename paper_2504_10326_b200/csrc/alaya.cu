@@ -365,12 +365,43 @@ int alaya_window_append(const alaya_params* p, const alaya_seq* seqs, int batch,
   return launch_pdl("window_commit_kernel", window_commit_kernel, 1, 128, 0, st, bt);  // ++*d_w
 }
 
+namespace {
+int dipr_attention_impl(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_k_new,
+                        const float* d_v_new, const float* d_q, float* d_out, void* d_ws, size_t ws_bytes,
+                        void* stream);
+}
+
 int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q,
                          float* d_out, void* d_ws, size_t ws_bytes, void* stream) {
+  return dipr_attention_impl(p, seqs, batch, nullptr, nullptr, d_q, d_out, d_ws, ws_bytes, stream);
+}
+
+int alaya_dipr_attention_update(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_k_new,
+                                const float* d_v_new, const float* d_q, float* d_out, void* d_ws,
+                                size_t ws_bytes, void* stream) {
+  if (!d_k_new || !d_v_new) return fail(ALAYA_ERR_ARG, "null k/v");
+  return dipr_attention_impl(p, seqs, batch, d_k_new, d_v_new, d_q, d_out, d_ws, ws_bytes, stream);
+}
+
+}  // extern "C"
+
+namespace {
+int dipr_attention_impl(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_k_new,
+                        const float* d_v_new, const float* d_q, float* d_out, void* d_ws, size_t ws_bytes,
+                        void* stream) {
   Call c;
   int rc = prepare(p, seqs, batch, d_ws, ws_bytes, stream, &c);
   if (rc) return rc;
   if (!d_q || !d_out) return fail(ALAYA_ERR_ARG, "null q/out");
+  if (d_k_new) {
+    for (int b = 0; b < batch; ++b) {
+      if (seqs[b].d_w) return fail(ALAYA_ERR_UNSUPPORTED, "seq %d: update+attention needs host window counts", b);
+      if (seqs[b].w < 1 || !seqs[b].wk || !seqs[b].wv)
+        return fail(ALAYA_ERR_ARG, "seq %d: update+attention needs a window ring with the new row counted", b);
+    }
+    c.bt.app_k = d_k_new;
+    c.bt.app_v = d_v_new;
+  }
   for (int b = 0; b < batch; ++b)
     if (seqs[b].prefix_len + seqs[b].w == 0) return fail(ALAYA_ERR_ARG, "attention on an empty session");
   c.bt.win_in_prep = 1;  // window partials computed by prep, off the attend's tail
@@ -388,6 +419,9 @@ int alaya_dipr_attention(const alaya_params* p, const alaya_seq* seqs, int batch
   if ((rc = c.st.attend(c.bt, d_q, nullptr, c.ws, 1, c.stream, 0))) return rc;
   return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);
 }
+}  // namespace
+
+extern "C" {
 
 int alaya_sharded_step(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q,
                        void* const* bufs, int n_ranks, int rank, int64_t cap_floats, unsigned long long epoch,

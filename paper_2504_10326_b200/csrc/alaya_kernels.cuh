@@ -1182,6 +1182,17 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
   if (lane == 0)
 #pragma unroll
     for (int j = 0; j < G; ++j) red[warp][j] = best[j];
+  if (bt.app_k) {  // Session.update of this call: the new row of ring (b, h) first
+    T* wk = const_cast<T*>(reinterpret_cast<const T*>(s.wk)) + (size_t)h * s.whs + (size_t)(s.w - 1) * D;
+    T* wv = const_cast<T*>(reinterpret_cast<const T*>(s.wv)) + (size_t)h * s.whs + (size_t)(s.w - 1) * D;
+    const float* kn = bt.app_k + ((size_t)b * bt.Hkv + h) * D;
+    const float* vn = bt.app_v + ((size_t)b * bt.Hkv + h) * D;
+    for (int e = threadIdx.x; e < D; e += blockDim.x) {
+      if constexpr (std::is_same_v<T, float>) { wk[e] = kn[e]; wv[e] = vn[e]; }
+      else { wk[e] = __float2bfloat16_rn(kn[e]); wv[e] = __float2bfloat16_rn(vn[e]); }
+    }
+    __syncthreads();  // (the window partial below reads the row)
+  }
   if (bt.win_in_prep) prep_window<T, D, G>(bt, ws, qr, b, h, a0, na, b0, nbw, lane, warp);
   __syncthreads();
   if (async) {  // seeds join the running max once the header is zeroed

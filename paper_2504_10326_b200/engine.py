@@ -198,13 +198,29 @@ class Call:
             raise ValueError(f"q must be {(self.B, p.n_query_heads, p.dim)}, got {tuple(q.shape)}")
         return q.to(device=self.device, dtype=torch.float32).contiguous()
 
-    def dipr_attention(self, q: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    def dipr_attention(self, q: torch.Tensor, out: torch.Tensor | None = None,
+                       append: tuple[torch.Tensor, torch.Tensor] | None = None) -> torch.Tensor:
+        """DIPR retrieval + sparse attention for the batch. ``append=(k, v)``
+        (``[B, Hkv, d]`` fp32): first write them as window row ``w - 1`` of every
+        sequence (``Session.update``; the sequences' ``w`` already count the row),
+        inside the same call (``alaya_dipr_attention_update``)."""
         q = self._q(q)
         if out is None:
             out = torch.empty_like(q)
-        check(self.lib.alaya_dipr_attention(ctypes.byref(self.params), self.seqs, self.B,
-                                            q.data_ptr(), out.data_ptr(), self.ws.data_ptr(),
-                                            self.ws_bytes, self.stream))
+        if append is None:
+            check(self.lib.alaya_dipr_attention(ctypes.byref(self.params), self.seqs, self.B,
+                                                q.data_ptr(), out.data_ptr(), self.ws.data_ptr(),
+                                                self.ws_bytes, self.stream))
+        else:
+            p = self.params
+            kn, vn = (t.to(device=self.device, dtype=torch.float32).contiguous() for t in append)
+            if kn.shape != (self.B, p.n_kv_heads, p.dim) or vn.shape != kn.shape:
+                raise ValueError(f"k/v must be {(self.B, p.n_kv_heads, p.dim)}")
+            check(self.lib.alaya_dipr_attention_update(ctypes.byref(self.params), self.seqs, self.B,
+                                                       kn.data_ptr(), vn.data_ptr(), q.data_ptr(),
+                                                       out.data_ptr(), self.ws.data_ptr(),
+                                                       self.ws_bytes, self.stream))
+            self._kv_keep = (kn, vn)
         self._q_keep = q
         return out
 

@@ -125,6 +125,7 @@ class Session:
         self.generated_token_ids.append(int(token_id))
 
     def window_arrays(self, layer: int, kv_head: int):
+        self._store._flush(layer)
         w = self._wlen[layer]
         d = self._store.shape.dim
         if w == 0:
@@ -146,6 +147,7 @@ class Session:
         cap = 0 if self._wk is None else self._wk.shape[2]
         if need <= cap:
             return
+        st._flush_all()  # the rings are copied below
         new_cap = max(64, cap * 2, need)
         sh = (st.shape.n_layers, st.shape.n_kv_heads, new_cap, st.shape.dim)
         wk = torch.zeros(sh, dtype=st.kv_dtype, device=st.device)
@@ -162,6 +164,7 @@ class Session:
                              _rows(k)[None] if not isinstance(k, torch.Tensor) else k[None],
                              _rows(v)[None] if not isinstance(v, torch.Tensor) else v[None], layer)
         shape = self._store.shape
+        self._store._flush(layer)
         w = self._wlen[layer]
         k_views, v_views = [], []
         for h in range(shape.n_kv_heads):
@@ -192,7 +195,12 @@ class Session:
             s._ensure_window(s._wlen[layer] + 1)
         kd = _to_device(k, st.device, torch.float32)
         vd = _to_device(v, st.device, torch.float32)
-        st._append(sessions, layer, kd, vd)
+        # the append is deferred to this layer's next attention call, which writes the
+        # rows in its first kernel (alaya_dipr_attention_update); any earlier reader of
+        # the rings flushes it (ContextStore._flush)
+        st._flush(layer)
+        st._pending[layer] = (list(sessions), kd, vd, [s._wlen[layer] for s in sessions],
+                              torch.cuda.current_stream(st.device))
         for b, s in enumerate(sessions):
             s._wlen[layer] += 1
             if st.log_queries:
@@ -238,15 +246,25 @@ class Session:
         calls = []
         for key, idx in groups.items():
             if key[0] in ("topk", "diprs"):
+                st._flush(layer)
                 for c0 in range(0, len(idx), _lib.MAX_BATCH):
                     part = idx[c0:c0 + _lib.MAX_BATCH]
                     Session._topk_group([sessions[i] for i in part], part, key, layer, qd, out)
                 continue
             _, beta, wi, wl = key
+            pend = st._pending.get(layer)
+            fuse = (pend is not None and len(groups) == 1 and len(sessions) <= _lib.MAX_BATCH
+                    and len(pend[0]) == len(sessions) and all(a is b for a, b in zip(pend[0], sessions)))
+            if not fuse:
+                st._flush(layer)
             for c0 in range(0, len(idx), _lib.MAX_BATCH):
                 part = idx[c0:c0 + _lib.MAX_BATCH]
                 call = st._call_for([sessions[i] for i in part], layer, beta, wi, wl)
-                if len(part) == len(sessions):
+                if fuse:  # Session.update's rows written by this call's first kernel
+                    del st._pending[layer]
+                    st._pending_on_stream(pend)
+                    call.dipr_attention(qd, out=out, append=(pend[1], pend[2]))
+                elif len(part) == len(sessions):
                     call.dipr_attention(qd, out=out)
                 else:
                     sel = torch.tensor(part, device=st.device)
@@ -418,6 +436,7 @@ class Session:
         return plan
 
     def full_kv(self, layer: int, head: int):
+        self._store._flush(layer)
         bk, bv = self._base_arrays(layer, head)
         w = self._wlen[layer]
         if w == 0:
@@ -441,6 +460,7 @@ class ContextStore:
         self.log_queries = log_queries
         self.contexts: dict[str, ContextRecord] = {}
         self._calls: dict = {}
+        self._pending: dict = {}  # layer -> deferred Session.update append (update_batch)
         self._plan_cache: dict = {}
         self._planner_cfg = self.config.planner_config()
         self.root = Path(root) if root is not None else None
@@ -511,6 +531,7 @@ class ContextStore:
             keys[:, :, :p] = session.base.keys[:, :, :p]
             values[:, :, :p] = session.base.values[:, :, :p]
         if w:
+            self._flush_all()
             keys[:, :, p:] = session._wk[:, :, :w]
             values[:, :, p:] = session._wv[:, :, :w]
         return self.import_context(token_ids, keys, values)
@@ -616,9 +637,28 @@ class ContextStore:
                                          for l in range(self.shape.n_layers)])
         return record.bounds
 
-    def _append(self, sessions: list["Session"], layer: int, kd: torch.Tensor, vd: torch.Tensor):
-        """One alaya_window_append for the batch; descriptors cached per (layer,
-        sessions) and rebuilt only when a window ring was reallocated."""
+    def _pending_on_stream(self, pend) -> None:
+        """A deferred append consumed on another stream than update_batch's: its
+        inputs were produced there (rare; the host waits for that stream)."""
+        if pend[4] != torch.cuda.current_stream(self.device):
+            pend[4].synchronize()
+
+    def _flush(self, layer: int) -> None:
+        """Launch this layer's deferred Session.update append (if any)."""
+        pend = self._pending.pop(layer, None)
+        if pend is not None:
+            self._pending_on_stream(pend)
+            self._append(pend[0], layer, pend[1], pend[2], pend[3])
+
+    def _flush_all(self) -> None:
+        for layer in list(self._pending):
+            self._flush(layer)
+
+    def _append(self, sessions: list["Session"], layer: int, kd: torch.Tensor, vd: torch.Tensor,
+                rows: list[int]):
+        """One alaya_window_append for the batch (row ``rows[i]`` of session i's
+        ring); descriptors cached per (layer, sessions) and rebuilt only when a
+        window ring was reallocated."""
         sig = tuple(id(s._wk) for s in sessions)
         key = ("append", layer, tuple(id(s) for s in sessions))
         hit = self._calls.get(key)
@@ -631,8 +671,8 @@ class ContextStore:
                 self._calls.clear()
             self._calls[key] = hit
         arr = hit[1]
-        for i, s in enumerate(sessions):
-            arr[i].w = s._wlen[layer]
+        for i in range(len(sessions)):
+            arr[i].w = rows[i]
         engine.window_append_raw(arr, len(sessions), self._append_params(), kd, vd)
 
     def _append_params(self):
