@@ -124,7 +124,9 @@ typedef struct {
   int32_t r;
 } alaya_block_index;
 
-#define ALAYA_MAX_BATCH 128
+#ifndef ALAYA_MAX_BATCH
+#define ALAYA_MAX_BATCH 32
+#endif
 #define ALAYA_PARTIAL_STRIDE(dim) ((dim) + 2) /* (m, l, acc[dim]) per query head */
 
 const char* alaya_last_error(void);

@@ -31,7 +31,7 @@ SCAN_AUTO = 0
 SCAN_CUDA_CORE = 1
 SCAN_TCGEN05 = 2
 
-MAX_BATCH = 128
+MAX_BATCH = 32  # include/alaya.h ALAYA_MAX_BATCH (kernel-parameter space: small batches launch fast)
 
 # every symbol include/alaya.h declares (checked by tests/test_boundary.py)
 EXPORTS = (

@@ -34,7 +34,7 @@ constexpr int kBoxBytes = kTileBytes / 2;        // 64 columns x 128 rows
 #endif
 constexpr int kThreadsTc = ALAYA_PUB_WARP ? 224 : 192;  // producer, MMA, 4 epilogue warps[, publisher]
 constexpr int kPubWarp = 6;
-constexpr int kMaxMaps = 128;
+constexpr int kMaxMaps = ALAYA_MAX_BATCH;  // one tensor map per distinct K slab
 
 struct Maps {
   CUtensorMap m[kMaxMaps];

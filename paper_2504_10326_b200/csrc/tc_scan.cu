@@ -3,6 +3,7 @@
 // per SM.
 #include <cudaTypedefs.h>
 
+#include <cmath>
 #include <cstdlib>
 #include <mutex>
 
@@ -52,12 +53,15 @@ int launch_s(const Batch& bt, const tc::Maps& maps, const float* q, const Ws& ws
   const size_t sm = tc::tc_smem_bytes(G, S);
   // persistent, chunks handed out dynamically; `less` SMs run one scan CTA instead
   // of two so attend CTAs fit beside it (an attend CTA cannot share an SM with two
-  // scan CTAs: registers), more of them as the attend work grows with the number of
-  // (sequence, kv head) groups (measured at 128K, profiles/r02/grid_less_v29.jsonl:
-  // B=1 best at 24-48, B=4 at 48-74, B=8 at 110). ALAYA_TC_GRID_LESS overrides.
+  // scan CTAs: registers), more of them as the call's work grows. Measured optima
+  // (profiles/r02/grid_less_v29.jsonl, grid_less_v35.jsonl), in units of 128K
+  // tokens summed over the batch: 1 -> 24-48, 2 (32K x 8) -> 48, 4 -> 48-74,
+  // 8 -> 110, 16 -> >= 110. ALAYA_TC_GRID_LESS overrides.
   static const int less_env = env_int("ALAYA_TC_GRID_LESS", -1);
-  const int groups = bt.B * bt.Hkv;
-  const int less = less_env >= 0 ? less_env : std::min(110, 24 + 3 * groups / 2);
+  double units = 0.0;
+  for (int b = 0; b < bt.B; ++b) units += (double)bt.s[b].n / 131072.0;
+  const int less = less_env >= 0 ? less_env
+                                 : std::min(140, (int)(24.0 + 22.0 * std::log2(std::max(1.0, units))));
   const int grid = std::min(bt.total_chunks, std::max(num_sms(), ctas_per_sm * num_sms() - less));
   if (bt.gfmt) {
     static bool attr = false;
