@@ -68,7 +68,8 @@ class ContextRecord:
     shape: ModelShape
     plans: dict[int, Plan]
     indexes: dict = field(default_factory=dict)
-    bounds: torch.Tensor | None = None  # [L, Hkv, blocks, 2, d] coarse block index (block filter)
+    bounds: torch.Tensor | None = None  # [L, Hkv, blocks, 5, d] coarse block index (block filter)
+    locality: list | None = None  # per layer: median block radius / median key norm
     block_reps: dict = field(default_factory=dict)  # layer -> [Hkv, blocks, r, d] (BlockIndex)
     graphs: dict = field(default_factory=dict)  # layer -> (offsets [Hkv,n+1], nbrs [Hkv,E], entry [Hkv])
 
@@ -374,14 +375,13 @@ class Session:
         """Identity of what _seq_view would describe, without building tensors."""
         p = self.reused_prefix_len if self.base is not None else 0
         w = self._wlen[layer]
-        return (id(self.base) if p else 0, p, id(self._wk) if w else 0,
-                bool(p and self._store.config.block_filter))
+        return (id(self.base) if p else 0, p, id(self._wk) if w else 0)
 
-    def _seq_view(self, layer: int) -> engine.SeqView:
+    def _seq_view(self, layer: int, block_filter: bool = False) -> engine.SeqView:
         p = self.reused_prefix_len if self.base is not None else 0
         w = self._wlen[layer]
         bnd = None
-        if p and self._store.config.block_filter:
+        if p and block_filter:
             bnd = self._store._bounds_for(self.base)[layer]
         return engine.SeqView(
             k=self.base.keys[layer] if p else None, v=self.base.values[layer] if p else None, n=p,
@@ -683,10 +683,45 @@ class ContextStore:
                                                self.kv_dtype, 0.0, 0, 0)
         return ap
 
+    # "auto" block filter: a context-layer qualifies when its 128-key blocks are tight
+    # (median block radius <= 0.8 x the median key norm: locality-ordered prefixes, e.g.
+    # tokens grouped by topic) and beta / sqrt(d) <= 5.5, where the blocks' box / ball
+    # bounds fall below max - beta. Measured at 128K (profiles/r01_sweep_config34_v17.jsonl):
+    # locality data keeps ~24 % of the blocks at beta <= 50 (B=4 232 -> 175 us) and none
+    # at beta = 110 (+19 %); on the reference generator's unordered data nothing prunes
+    # at any beta (+20 %), and its radius ratio is ~1.5.
+    _AUTO_RADIUS_RATIO = 0.8
+    _AUTO_BETA_PER_SQRT_D = 5.5
+
+    def _filter_for(self, sessions: list["Session"], layer: int, beta: float) -> bool:
+        mode = self.config.block_filter
+        if mode is not True and mode != "auto":
+            return False
+        bases = [s.base for s in sessions if s.base is not None and s.reused_prefix_len]
+        if not bases:
+            return False
+        if mode is True:
+            return True
+        if not (beta / math.sqrt(self.shape.dim) <= self._AUTO_BETA_PER_SQRT_D):
+            return False
+        return all(self._locality(b)[layer] <= self._AUTO_RADIUS_RATIO for b in bases)
+
+    def _locality(self, record: ContextRecord) -> list:
+        """Per layer: median block radius / median block representative norm (one
+        host sync when the block index is first built)."""
+        if record.locality is None:
+            bnd = self._bounds_for(record)                      # [L, Hkv, blocks, 5, d]
+            radius = bnd[:, :, :, 4, 0].float().flatten(1)      # row 4, element 0
+            rep = bnd[:, :, :, 3, :].float().norm(dim=-1).flatten(1)
+            ratio = radius.median(dim=1).values / rep.median(dim=1).values.clamp_min(1e-30)
+            record.locality = ratio.cpu().tolist()
+        return record.locality
+
     def _call_for(self, sessions: list["Session"], layer: int, beta: float, wi: int, wl: int):
         """Validated C-ABI descriptors for (layer, sessions), cached across steps:
         only the window row counts change between decode steps."""
-        sig = tuple(s._view_sig(layer) for s in sessions)
+        flt = self._filter_for(sessions, layer, beta)
+        sig = tuple(s._view_sig(layer) for s in sessions) + (flt,)
         key = (layer, tuple(id(s) for s in sessions), beta, wi, wl)
         hit = self._calls.get(key)
         if hit is not None and hit[0] == sig:  # (the entry holds the objects the ids name)
@@ -694,11 +729,11 @@ class ContextStore:
             for i, s in enumerate(sessions):
                 call.seqs[i].w = s._wlen[layer]
             return call
-        views = [s._seq_view(layer) for s in sessions]
+        views = [s._seq_view(layer, flt) for s in sessions]
         sh = self.shape
         params = engine.make_params(sh.n_query_heads, sh.n_kv_heads, sh.dim, self.kv_dtype, beta,
                                     wi, wl, self.config.chunk, _SCAN_KIND[self.config.scan_kernel],
-                                    int(self.config.block_filter))
+                                    int(flt))
         call = engine.Call(views, params, self.kv_dtype, self.device)
         if len(self._calls) > 4096:
             self._calls.clear()

@@ -110,3 +110,35 @@ def test_filter_keeps_everything_on_reference_generator(cuda_ok):
     assert kept == total
     ref, _, _ = O.session_attention_flat(q, keys[0], vals[0], None, None, 110.0)
     assert rel(out, ref) <= 1e-5
+
+
+@pytest.mark.parametrize("ordered,beta,want", [(True, 20.0, True), (True, 110.0, False),
+                                               (False, 20.0, False)])
+def test_auto_filter_decision(cuda_ok, ordered, beta, want):
+    """block_filter="auto" (the default): on only for a context whose 128-key blocks
+    are tight (locality) at a beta small enough for their bounds to prune; results
+    equal the oracle either way."""
+    import paper_2504_10326_b200 as P
+    n, hkv, g, d = 20000, 2, 4, 128
+    if ordered:
+        keys, vals, centers = locality_context(n, hkv, d, seed=7)
+        tok = np.arange(n)
+    else:
+        tok, keys, vals, centers, _ = O.make_context(n, 1, hkv, d, seed=7)
+    keys, vals = O.bf16_round(keys), O.bf16_round(vals)
+    cfg = P.EngineConfig(beta=beta, first_layers=(0,), short_context_threshold=0,
+                         kv_dtype="bfloat16")
+    assert cfg.block_filter == "auto"
+    db = P.ContextStore(P.ModelShape(1, hkv * g, hkv, d), cfg)
+    db.import_context(tok, keys, vals)
+    s, _ = db.create_session(tok)
+    assert db._filter_for([s], 0, beta) is want
+    q = (centers[:hkv * g] + 0.1).astype(np.float32)
+    out = s.attention(q, 0)
+    call = next(iter(db._calls.values()))[1]
+    assert bool(call.params.block_filter) is want
+    if want:
+        kept, total = call.block_stats()
+        assert kept < total
+    ref, _, _ = O.session_attention_flat(q, keys[0], vals[0], None, None, beta)
+    assert rel(out, ref) <= 1e-5

@@ -179,3 +179,12 @@ def test_package_alpha_to_beta_matches_oracle():
     for bad in ((0.0, 8), (1.5, 8), (0.5, 0)):
         with pytest.raises(ValueError):
             D.alpha_to_beta(*bad)
+
+
+def test_engine_config_block_filter_modes():
+    from paper_2504_10326_b200.config import EngineConfig
+    assert EngineConfig().block_filter == "auto"
+    for v in (True, False, "auto"):
+        assert EngineConfig(block_filter=v).block_filter == v
+    with pytest.raises(ValueError):
+        EngineConfig(block_filter="sometimes")
