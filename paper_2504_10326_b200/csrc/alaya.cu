@@ -111,10 +111,16 @@ int build_batch(const alaya_params* p, const alaya_seq* seqs, int B, Batch* bt) 
   bt->inv_sqrt_d = (float)(1.0 / std::sqrt((double)p->dim));
   bt->block_filter = p->block_filter ? 1 : 0;
   {  // attend task split threshold; ALAYA_SPLIT overrides (diagnostics)
-    const char* e = getenv("ALAYA_SPLIT");
-    bt->split = (e && *e) ? atoi(e) : std::max(256, chunk / 4);
-    const char* sd = getenv("ALAYA_SEED");  // diagnostics: 0 = no running-max seed
-    bt->seed = (sd && *sd) ? atoi(sd) : 1;
+    static const int split_env = [] {
+      const char* e = getenv("ALAYA_SPLIT");
+      return (e && *e) ? atoi(e) : -1;
+    }();
+    static const int seed_env = [] {  // diagnostics: 0 = no running-max seed
+      const char* sd = getenv("ALAYA_SEED");
+      return (sd && *sd) ? atoi(sd) : 1;
+    }();
+    bt->split = split_env >= 0 ? split_env : std::max(256, chunk / 4);
+    bt->seed = seed_env;
   }
   int cb = 0;
   for (int b = 0; b < B; ++b) {

@@ -110,6 +110,18 @@ int build_maps(const Batch& bt, const alaya_seq* seqs, tc::Maps& maps) {
       if (seqs[a].n && seqs[a].k == seqs[b].k) found = maps.map_of_seq[a];
     if (found >= 0) { maps.map_of_seq[b] = (int16_t)found; continue; }
     const cuuint64_t rows = (cuuint64_t)bt.Hkv * (seqs[b].head_stride / 128);
+    // encoded maps are cached per (slab, rows): decode steps re-use the same slabs
+    struct Cached { const void* k; cuuint64_t rows; CUtensorMap m; };
+    static thread_local Cached cache[64];
+    static thread_local int cache_next = 0;
+    const Cached* hit = nullptr;
+    for (int i = 0; i < 64 && !hit; ++i)
+      if (cache[i].k == seqs[b].k && cache[i].rows == rows) hit = &cache[i];
+    if (hit) {
+      maps.m[nmaps] = hit->m;
+      maps.map_of_seq[b] = (int16_t)nmaps++;
+      continue;
+    }
     cuuint64_t gdim[2] = {128, rows};
     cuuint64_t gstride[1] = {256};
     cuuint32_t box[2] = {64, (cuuint32_t)tc::kTileKeys};
@@ -118,6 +130,8 @@ int build_maps(const Batch& bt, const alaya_seq* seqs, tc::Maps& maps) {
                      gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_128B, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(ALAYA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    cache[cache_next] = {seqs[b].k, rows, maps.m[nmaps]};
+    cache_next = (cache_next + 1) % 64;
     maps.map_of_seq[b] = (int16_t)nmaps++;
   }
   return ALAYA_OK;
@@ -168,7 +182,8 @@ int launch_tc_scan(const Batch& bt_in, const alaya_seq* seqs, const float* q, co
   if (bt_in.total_chunks == 0) return ALAYA_OK;
   static thread_local Batch bt;
   bt = bt_in;
-  bt.dbg = env_int("ALAYA_TC_DBG", 0);
+  static const int dbg = env_int("ALAYA_TC_DBG", 0);
+  bt.dbg = dbg;
   static thread_local tc::Maps maps;  // ~19 KB: keep off the stack
   int rc = build_maps(bt, seqs, maps);
   if (rc) return rc;

@@ -178,11 +178,13 @@ class Call:
         call issued on another stream switches to that stream's workspace, so two
         streams never race on one header."""
         if self._ws_shared:
-            st = torch.cuda.current_stream(self.device).cuda_stream
-            if st != self._ws_stream:
-                self._ws = _WS.get(self._nbytes, self.device, st)
-                self._ws_stream, self.ws_bytes = st, self._ws.numel()
+            self._bind(torch.cuda.current_stream(self.device).cuda_stream)
         return self._ws
+
+    def _bind(self, st: int) -> None:
+        if self._ws_shared and st != self._ws_stream:
+            self._ws = _WS.get(self._nbytes, self.device, st)
+            self._ws_stream, self.ws_bytes = st, self._ws.numel()
 
     @ws.setter
     def ws(self, t: torch.Tensor) -> None:  # a caller-owned workspace (e.g. a captured graph's)
@@ -196,6 +198,8 @@ class Call:
         p = self.params
         if q.shape != (self.B, p.n_query_heads, p.dim):
             raise ValueError(f"q must be {(self.B, p.n_query_heads, p.dim)}, got {tuple(q.shape)}")
+        if q.dtype == torch.float32 and q.is_cuda and q.is_contiguous() and q.device == self.device:
+            return q
         return q.to(device=self.device, dtype=torch.float32).contiguous()
 
     def dipr_attention(self, q: torch.Tensor, out: torch.Tensor | None = None,
@@ -207,10 +211,12 @@ class Call:
         q = self._q(q)
         if out is None:
             out = torch.empty_like(q)
+        st = torch.cuda.current_stream(self.device).cuda_stream  # (once per call: the hot path)
+        self._bind(st)
         if append is None:
             check(self.lib.alaya_dipr_attention(ctypes.byref(self.params), self.seqs, self.B,
-                                                q.data_ptr(), out.data_ptr(), self.ws.data_ptr(),
-                                                self.ws_bytes, self.stream))
+                                                q.data_ptr(), out.data_ptr(), self._ws.data_ptr(),
+                                                self.ws_bytes, st))
         else:
             p = self.params
             kn, vn = (t.to(device=self.device, dtype=torch.float32).contiguous() for t in append)
@@ -218,8 +224,8 @@ class Call:
                 raise ValueError(f"k/v must be {(self.B, p.n_kv_heads, p.dim)}")
             check(self.lib.alaya_dipr_attention_update(ctypes.byref(self.params), self.seqs, self.B,
                                                        kn.data_ptr(), vn.data_ptr(), q.data_ptr(),
-                                                       out.data_ptr(), self.ws.data_ptr(),
-                                                       self.ws_bytes, self.stream))
+                                                       out.data_ptr(), self._ws.data_ptr(),
+                                                       self.ws_bytes, st))
             self._kv_keep = (kn, vn)
         self._q_keep = q
         return out
