@@ -541,9 +541,9 @@ int alaya_selected(const alaya_params* p, const alaya_seq* seqs, int batch, int6
     }
   }
   const dim3 grid(batch * c.bt.Hq, std::max(1, (max_nch + kWarps - 1) / kWarps));  // a warp per chunk
-  selected_kernel<<<grid, kThreads, sm, c.stream>>>(c.bt, c.ws, d_ids, cap, d_selected,
-                                                    d_retrieved);  // (format: ws.mode)
-  return cuda_check("selected_kernel");
+  // PDL: launched while the call's combine finishes; waits for it before reading
+  return launch_pdl("selected_kernel", selected_kernel, grid, dim3(kThreads), sm, c.stream, c.bt, c.ws, d_ids,
+                    cap, d_selected, d_retrieved);  // (format: ws.mode)
 }
 
 int alaya_topk(const alaya_params* p, const alaya_seq* seqs, int batch, const float* d_q, int k,

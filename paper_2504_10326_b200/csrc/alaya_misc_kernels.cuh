@@ -86,6 +86,8 @@ __global__ void __launch_bounds__(kThreads) selected_kernel(const __grid_constan
   __shared__ unsigned bm[kWarps][kMaxWords];
   __shared__ int wsum[kWarps], wret[kWarps];
   extern __shared__ int chunk_base[];   // [nch] exclusive prefix of selected counts
+  pdl_wait();     // the call's attend/combine are complete
+  pdl_trigger();  // (the next call's prep waits for this grid before zeroing the header)
   const int row = blockIdx.x;
   const int b = row / bt.Hq, qh = row - b * bt.Hq;
   const int h = qh / bt.G, j = qh - h * bt.G;

@@ -270,16 +270,16 @@ class Session:
                 else:
                     sel = torch.tensor(part, device=st.device)
                     out.index_copy_(0, sel, call.dipr_attention(qd.index_select(0, sel)))
-                seqs = [sessions[i]._seq_view(layer) for i in part] if st.config.diagnostics else []
                 if st.config.diagnostics:
-                    cap = max(1, max(sv.n for sv in seqs))
-                    ids, nsel, nret = call.selected(cap)
+                    plens = [sessions[i].reused_prefix_len if sessions[i].base is not None else 0
+                             for i in part]
+                    ids, nsel, nret = call.selected(max(1, max(plens)))
                     hq = shape.n_query_heads
                     for j, i in enumerate(part):
                         s = sessions[i]
                         r = slice(j * hq, (j + 1) * hq)
-                        s._diag = (layer, s.active_plan(layer), ids[r], nsel[r], nret[r],
-                                   s.reused_prefix_len if s.base is not None else 0, wi, wl)
+                        # (the views are sliced when last_diagnostics is read)
+                        s._diag = (layer, s.active_plan(layer), ids, nsel, nret, plens[j], wi, wl, r)
                 calls.append(call)
         if as_numpy:
             res = out.cpu().numpy()
@@ -342,7 +342,8 @@ class Session:
                               "window_base": window.tolist(), "retrieved": int(cnt[qh]),
                               "query_head": qh})
             return {"layer": layer, "plan": active, "heads": heads}
-        layer, active, ids, nsel, nret, p, wi, wl = self._diag
+        layer, active, ids, nsel, nret, p, wi, wl, r = self._diag
+        ids, nsel, nret = ids[r], nsel[r], nret[r]
         nsel, nret = nsel.cpu().numpy(), nret.cpu().numpy()
         width = int(nsel.max()) if nsel.size else 0  # rows are written up to their count only
         ids = ids[:, :max(width, 1)].cpu().numpy()
