@@ -18,9 +18,15 @@ bool pdl_enabled();
 // Launch with the programmatic-dependent-launch attribute (ALAYA_PDL=0 turns
 // it off). Every kernel launched this way calls pdl_wait() before touching
 // data written by earlier work on the stream.
+// Every kernel of the path prefers the maximum shared-memory carveout, so an SM
+// never has to drain to switch the L1 / shared split between consecutive kernels
+// (the tcgen05 scan needs the maximum). ALAYA_CARVEOUT=0 leaves the driver default.
+void prefer_max_smem(const void* kern);
+
 template <typename... KArgs, typename... Args>
 int launch_pdl(const char* what, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                cudaStream_t st, Args&&... args) {
+  prefer_max_smem(reinterpret_cast<const void*>(kern));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

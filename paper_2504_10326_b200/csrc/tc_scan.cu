@@ -152,6 +152,20 @@ bool tc_scan_eligible(const Batch& bt, int dtype, const alaya_seq* seqs) {
   return distinct <= tc::kMaxMaps && encode_fn() != nullptr;
 }
 
+void prefer_max_smem(const void* kern) {
+  static const int on = env_int("ALAYA_CARVEOUT", 1);
+  if (!on) return;
+  static std::mutex mu;
+  static const void* done[512];
+  static int ndone = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < ndone; ++i)
+    if (done[i] == kern) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  cudaGetLastError();  // (a kernel that cannot take the attribute keeps the default)
+  if (ndone < 512) done[ndone++] = kern;
+}
+
 bool pdl_enabled() {
   static const int on = env_int("ALAYA_PDL", 1);
   return on != 0;
