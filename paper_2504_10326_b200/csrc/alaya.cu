@@ -421,6 +421,13 @@ int dipr_attention_impl(const alaya_params* p, const alaya_seq* seqs, int batch,
       return rc;
     return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);
   }
+  if (!c.use_tc && cc_overlap_enabled()) {  // CUDA-core scan: persistent, attend beside it
+    c.bt.overlap = 1;
+    c.bt.persist = 1;
+    if ((rc = run_scan(c, d_q))) return rc;
+    if ((rc = c.st.attend_ovl(c.bt, d_q, c.ws, c.stream))) return rc;
+    return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);
+  }
   if ((rc = run_scan(c, d_q))) return rc;  // prep zeroed the status word and the ticket
   if ((rc = c.st.attend(c.bt, d_q, nullptr, c.ws, 1, c.stream, 0))) return rc;
   return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);

@@ -100,6 +100,7 @@ struct Batch {
   int32_t win_in_prep;  // prep_kernel computes the window partials (the attend skips window tasks)
   const float* app_k;   // != null: prep first writes row w-1 of every window ring from these
   const float* app_v;   //   ([B][Hkv][D] fp32; alaya_dipr_attention_update)
+  int32_t persist;      // CUDA-core scan: persistent grid, chunks in order from counters[9]
   int32_t gfmt;         // group candidate format: the tcgen05 scan writes one list per (chunk,
                         // quarter) of rows some head of the GQA group keeps, with all G scores;
                         // attend_grp_kernel gathers each V row once for the whole group

@@ -12,21 +12,16 @@ namespace alaya {
 int fail(int code, const char* fmt, ...);
 int num_sms();
 int cuda_check(const char* what);
+int persist_less(const Batch& bt);
 
 bool pdl_enabled();
 
 // Launch with the programmatic-dependent-launch attribute (ALAYA_PDL=0 turns
 // it off). Every kernel launched this way calls pdl_wait() before touching
 // data written by earlier work on the stream.
-// Every kernel of the path prefers the maximum shared-memory carveout, so an SM
-// never has to drain to switch the L1 / shared split between consecutive kernels
-// (the tcgen05 scan needs the maximum). ALAYA_CARVEOUT=0 leaves the driver default.
-void prefer_max_smem(const void* kern);
-
 template <typename... KArgs, typename... Args>
 int launch_pdl(const char* what, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                cudaStream_t st, Args&&... args) {
-  prefer_max_smem(reinterpret_cast<const void*>(kern));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -51,7 +46,16 @@ struct Stages {
     if (bt.total_chunks == 0) return ALAYA_OK;
     size_t sm = scan_smem(bt);
     cudaFuncSetAttribute(scan_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    return launch_pdl("scan_kernel", scan_kernel<T, D, G>, bt.total_chunks, kThreads, sm, st, bt, q, ws);
+    int grid = bt.total_chunks;
+    if (bt.persist) {  // one CTA fewer on `less` SMs: room for attend CTAs beside the scan
+      static int per_sm = 0;
+      if (per_sm == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_kernel<T, D, G>, kThreads, sm);
+        if (per_sm < 1) per_sm = 1;
+      }
+      grid = std::min(bt.total_chunks, std::max(num_sms(), per_sm * num_sms() - persist_less(bt)));
+    }
+    return launch_pdl("scan_kernel", scan_kernel<T, D, G>, grid, kThreads, sm, st, bt, q, ws);
   }
   static int prep(const Batch& bt, const float* q, const Ws& ws, cudaStream_t st) {
     // window partials in prep: one (m, l, acc) staging row per (warp, head)
@@ -91,6 +95,7 @@ struct Stages {
     }
     const long tasks = (long)bt.total_chunks * G + (bt.win_in_prep ? 0 : (long)bt.B * bt.Hq);
     const long blocks = std::min<long>((tasks + 3) / 4, (long)per_sm * num_sms());
+    if (blocks == 0) return ALAYA_OK;  // (no base chunks, window partials from prep)
     return launch_pdl("attend_ovl_kernel", attend_ovl_kernel<T, D, G>, (unsigned)blocks, kOvlThreads, 0,
                       st, bt, q, ws);
   }
@@ -174,6 +179,7 @@ int launch_tc_scan(const Batch& bt, const alaya_seq* seqs, const float* q, const
                    cudaStream_t st);
 bool overlap_enabled();
 bool gfmt_enabled(const Batch& bt);
+bool cc_overlap_enabled();
 int64_t diprs_row_bytes(int max_n, int cap);
 int launch_diprs(const Batch& bt, int dtype, const alaya_graph* graphs, const float* q, int l0, int floor_mode,
                  const float* floors, int cap, int64_t* ids, int64_t out_cap, int32_t* count, int32_t* explored,

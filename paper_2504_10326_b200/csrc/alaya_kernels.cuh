@@ -31,9 +31,8 @@ __device__ __forceinline__ void tr_level(float (&a)[P], int mask, bool upper) {
 // Stage 1: scan (reference: core.py:64-67 inner_products, dipr.py:63-64 max)
 // ---------------------------------------------------------------------------
 template <typename T, int D, int G>
-__global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
-    scan_kernel(const __grid_constant__ Batch bt, const float* __restrict__ q, Ws ws) {
-  extern __shared__ float smem[];
+__device__ __forceinline__ void scan_chunk(const Batch& bt, const float* __restrict__ q, const Ws& ws,
+                                           const int c, float* smem) {
   constexpr int DPL = D / 16;  // dims per lane (half-warp per key)
   const int chunk = bt.chunk;
   float* sc = smem;                        // [G][chunk] scores
@@ -41,10 +40,8 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
   float* thr = red + kWarps * G;           // [G]
   int* wc = reinterpret_cast<int*>(thr + G);  // [kWarps][G]
 
-  pdl_wait();
-  pdl_trigger();  // after the wait: see alaya_tc.cuh (attend_ovl relies on it)
   int b, h, ci;
-  decode_chunk(bt, blockIdx.x, b, h, ci);
+  decode_chunk(bt, c, b, h, ci);
   const KSeq& s = bt.s[b];
   const int t0 = ci * chunk;
   const int valid = min(chunk, s.n - t0);
@@ -126,7 +123,7 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
 
   // kept tiles (block filter), SUB steps each, double-buffered: load the next
   // step while computing the current one
-  const unsigned long long tmask = chunk_tiles(bt, ws, blockIdx.x, ntiles);
+  const unsigned long long tmask = chunk_tiles(bt, ws, c, ntiles);
   unsigned long long mrem = tmask;
   int tile_open = -1, sub_next = 0;
   auto pop = [&]() -> int {
@@ -183,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
     if (lane == 0) wc[warp * G + j] = cnt;
   }
   __syncthreads();
-  const size_t cbase = (size_t)blockIdx.x * G;
+  const size_t cbase = (size_t)c * G;
   const int quarter = warp >> 1;  // sub-list = position quarter (warps 2k, 2k+1)
 #pragma unroll
   for (int j = 0; j < G; ++j) {
@@ -222,6 +219,30 @@ __global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
       atomicAdd(&ws.group_done[b * bt.Hkv + h], 4);
       atomicAdd(&ws.counters[6], 4);
     }
+  }
+}
+
+
+// One CTA per chunk, or (bt.persist) a persistent grid taking chunks in increasing
+// order from the header counter, so the (sequence, kv head) groups complete in
+// order and the attend can run beside the scan (overlap mode).
+template <typename T, int D, int G>
+__global__ void __launch_bounds__(kThreads, (G <= 5 ? 2 : 1))
+    scan_kernel(const __grid_constant__ Batch bt, const float* __restrict__ q, Ws ws) {
+  extern __shared__ float smem[];
+  __shared__ int s_next;
+  pdl_wait();
+  pdl_trigger();  // after the wait: see alaya_tc.cuh (attend_ovl relies on it)
+  if (!bt.persist) {
+    scan_chunk<T, D, G>(bt, q, ws, (int)blockIdx.x, smem);
+    return;
+  }
+  for (int c = (int)blockIdx.x; c < bt.total_chunks;) {
+    if (threadIdx.x == 0) s_next = (int)gridDim.x + atomicAdd(&ws.counters[9], 1);
+    scan_chunk<T, D, G>(bt, q, ws, c, smem);
+    __syncthreads();  // shared scores / counts are reused by the next chunk; s_next is set
+    c = s_next;
+    __syncthreads();
   }
 }
 

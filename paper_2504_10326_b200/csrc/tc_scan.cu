@@ -152,20 +152,6 @@ bool tc_scan_eligible(const Batch& bt, int dtype, const alaya_seq* seqs) {
   return distinct <= tc::kMaxMaps && encode_fn() != nullptr;
 }
 
-void prefer_max_smem(const void* kern) {
-  static const int on = env_int("ALAYA_CARVEOUT", 1);
-  if (!on) return;
-  static std::mutex mu;
-  static const void* done[512];
-  static int ndone = 0;
-  std::lock_guard<std::mutex> lock(mu);
-  for (int i = 0; i < ndone; ++i)
-    if (done[i] == kern) return;
-  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-  cudaGetLastError();  // (a kernel that cannot take the attribute keeps the default)
-  if (ndone < 512) done[ndone++] = kern;
-}
-
 bool pdl_enabled() {
   static const int on = env_int("ALAYA_PDL", 1);
   return on != 0;
@@ -184,6 +170,20 @@ bool gfmt_enabled(const Batch& bt) {
   static const int mode = env_int("ALAYA_GFMT", -1);
   if (mode >= 0) return mode != 0;
   return bt.beta * bt.inv_sqrt_d >= 11.5f;
+}
+
+// CUDA-core scan (fp32 K/V, other dims) with the attend beside it: persistent scan
+// grid (ALAYA_OVERLAP_CC=0: one CTA per chunk, the attend after the scan)
+bool cc_overlap_enabled() {
+  static const int on = env_int("ALAYA_OVERLAP_CC", 1);
+  return on != 0;
+}
+int persist_less(const Batch& bt) {
+  static const int less_env = env_int("ALAYA_CC_GRID_LESS", -1);
+  if (less_env >= 0) return less_env;
+  double units = 0.0;
+  for (int b = 0; b < bt.B; ++b) units += (double)bt.s[b].n / 131072.0;
+  return std::min(140, (int)(24.0 + 22.0 * std::log2(std::max(1.0, units))));
 }
 
 bool overlap_enabled() {
