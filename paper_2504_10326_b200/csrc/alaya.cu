@@ -146,7 +146,7 @@ size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 struct Layout {
   size_t zero_bytes;
   size_t cscore_end;
-  size_t status, seeded, gmax, counters, cnt, selcnt, retcnt, part_l, part_acc, cidx, cscore, partbuf, smaxbuf,
+  size_t status, seeded, prepdone, gmax, counters, cnt, selcnt, retcnt, part_l, part_acc, cidx, cscore, partbuf, smaxbuf,
       keep, ovl_l, ovl_acc, ovl_sel, ovl_ret, heavy, ovlist, gidx, total;
 };
 
@@ -156,6 +156,7 @@ Layout layout_for(const Batch& bt) {
   size_t o = 0;
   L.status = o; o = align_up(o + 16);  // status, ready
   L.seeded = o; o = align_up(o + 8 * (size_t)bt.B * bt.Hkv);
+  L.prepdone = o; o = align_up(o + 8 * (size_t)bt.B * bt.Hkv);
   L.gmax = o; L.counters = o + 4 * rows;
   L.zero_bytes = 4 * rows + 64 + 4 * (size_t)bt.B * bt.Hkv;  // gmax, counters, group_done (prep_kernel)
   o = align_up(o + L.zero_bytes);
@@ -189,6 +190,7 @@ Ws carve(const Layout& L, void* base) {
   w.gidx = reinterpret_cast<int*>(c + L.gidx);
   w.ready = reinterpret_cast<unsigned long long*>(c + L.status + 8);
   w.seeded = reinterpret_cast<unsigned long long*>(c + L.seeded);
+  w.prepdone = reinterpret_cast<unsigned long long*>(c + L.prepdone);
   w.gmax = reinterpret_cast<uint32_t*>(c + L.gmax);
   w.counters = reinterpret_cast<int*>(c + L.counters);
   w.group_done = w.counters + 16;

@@ -146,6 +146,7 @@ struct Ws {
   int* gidx;        // [chunks][chunk] group format: candidate rows per (chunk, quarter) sub-list
   unsigned long long* ready;  // call id whose header prep has zeroed (next to status, never zeroed)
   unsigned long long* seeded;  // [B*Hkv] call id whose seeds of (seq, kv head) are in gmax (never zeroed)
+  unsigned long long* prepdone;  // [B*Hkv] call id whose prep CTA of (seq, kv head) has finished
   uint32_t* gmax;   // [B*Hq] order-preserving encoded running max
   int* counters;    // [16] right after gmax (zeroed by prep_kernel): [0] attend ticket,
                     // [2..3] block-filter kept/total, [6] epilogue-warp chunk publications

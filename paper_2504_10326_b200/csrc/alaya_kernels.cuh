@@ -839,7 +839,7 @@ __global__ void __launch_bounds__(CW * 32)
     // wait timed out still signs off -- a zeroed counter could lose that arrival)
     const unsigned long long tok = call_token(bt);
     for (int g = threadIdx.x; g < bt.B * bt.Hkv; g += blockDim.x)
-      while (ld_acquire_gpu_u64(ws.seeded + g) != tok) __nanosleep(64);
+      while (ld_acquire_gpu_u64(ws.prepdone + g) != tok) __nanosleep(64);
     __syncthreads();
   }
   if (threadIdx.x == 0) trace_rec(bt, 3, 2);
@@ -1203,20 +1203,9 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
   if (lane == 0)
 #pragma unroll
     for (int j = 0; j < G; ++j) red[warp][j] = best[j];
-  if (bt.app_k) {  // Session.update of this call: the new row of ring (b, h) first
-    T* wk = const_cast<T*>(reinterpret_cast<const T*>(s.wk)) + (size_t)h * s.whs + (size_t)(s.w - 1) * D;
-    T* wv = const_cast<T*>(reinterpret_cast<const T*>(s.wv)) + (size_t)h * s.whs + (size_t)(s.w - 1) * D;
-    const float* kn = bt.app_k + ((size_t)b * bt.Hkv + h) * D;
-    const float* vn = bt.app_v + ((size_t)b * bt.Hkv + h) * D;
-    for (int e = threadIdx.x; e < D; e += blockDim.x) {
-      if constexpr (std::is_same_v<T, float>) { wk[e] = kn[e]; wv[e] = vn[e]; }
-      else { wk[e] = __float2bfloat16_rn(kn[e]); wv[e] = __float2bfloat16_rn(vn[e]); }
-    }
-    __syncthreads();  // (the window partial below reads the row)
-  }
-  if (bt.win_in_prep) prep_window<T, D, G>(bt, ws, qr, b, h, a0, na, b0, nbw, lane, warp);
   __syncthreads();
-  if (async) {  // seeds join the running max once the header is zeroed
+  if (async) {  // seeds join the running max once the header is zeroed, then the group's
+                // seed flag goes up (the scan's epilogue starts its first chunk on it)
     __shared__ int s_ok;
     if (threadIdx.x == 0) {
       // bounded: a seed is optional (a lower bound), so a CTA that cannot see the
@@ -1234,8 +1223,26 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const __grid_constant__ 
       if (bt.seed && m > -INFINITY) atomicMax(&ws.gmax[b * bt.Hq + h * G + threadIdx.x], enc_max(m));
     }
     __syncthreads();
-    if (threadIdx.x == 0) {  // seeds of this group are in (combine waits on it)
+    if (threadIdx.x == 0)
       asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ws.seeded + blockIdx.x), "l"(call_token(bt))
+                   : "memory");
+  }
+  if (bt.app_k) {  // Session.update of this call: the new row of ring (b, h) first
+    T* wk = const_cast<T*>(reinterpret_cast<const T*>(s.wk)) + (size_t)h * s.whs + (size_t)(s.w - 1) * D;
+    T* wv = const_cast<T*>(reinterpret_cast<const T*>(s.wv)) + (size_t)h * s.whs + (size_t)(s.w - 1) * D;
+    const float* kn = bt.app_k + ((size_t)b * bt.Hkv + h) * D;
+    const float* vn = bt.app_v + ((size_t)b * bt.Hkv + h) * D;
+    for (int e = threadIdx.x; e < D; e += blockDim.x) {
+      if constexpr (std::is_same_v<T, float>) { wk[e] = kn[e]; wv[e] = vn[e]; }
+      else { wk[e] = __float2bfloat16_rn(kn[e]); wv[e] = __float2bfloat16_rn(vn[e]); }
+    }
+    __syncthreads();  // (the window partial below reads the row)
+  }
+  if (bt.win_in_prep) prep_window<T, D, G>(bt, ws, qr, b, h, a0, na, b0, nbw, lane, warp);
+  __syncthreads();
+  if (async) {
+    if (threadIdx.x == 0) {  // this CTA is done (window partial written; combine waits on it)
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ws.prepdone + blockIdx.x), "l"(call_token(bt))
                    : "memory");
       trace_rec(bt, 0, 1);
     }

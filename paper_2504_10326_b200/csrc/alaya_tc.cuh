@@ -564,10 +564,20 @@ __global__ void __launch_bounds__(kThreadsTc) __maxnreg__((scan_tc_maxreg<G, kSt
 #pragma unroll
       for (int j = 0; j < G; ++j) pre[j] = __ldcg(&ws.gmax[b * bt.Hq + h * G + j]);
     };
-    // (no wait for prep's seeds: whatever the header holds -- zero, a seed, other
-    // chunks' maxima -- is a lower bound of the max, and the chunk's own tile
-    // maxima tighten it from the first tile on; the seeds are picked up as they land)
+    // (later chunks do not wait: whatever the header holds -- a seed, other chunks'
+    // maxima -- is a lower bound of the max; the seeds matter most for the first chunk
+    // on locality-ordered prefixes, where a chunk-local bound keeps whole clusters)
     int c = read_id(0);
+    if (c >= 0 && bt.call_id) {  // the first chunk starts from its group's prep seed (bounded
+      int b, h, ci;            // wait; prep publishes the seeds before its window partials)
+      decode_chunk(bt, c, b, h, ci);
+      if (lane == 0) {
+        int polls = 0;
+        const unsigned long long tok = call_token(bt);
+        while (ld_acquire_gpu_u64(ws.seeded + b * bt.Hkv + h) != tok && ++polls < (1 << 16)) __nanosleep(64);
+      }
+      __syncwarp();
+    }
     if (c >= 0) load_pre(c);
     for (int k = 0; c >= 0; ++k) {
       int b, h;
