@@ -188,18 +188,20 @@ def test_sharded_attention_over_peer_exchange(cuda_ok):
         _lib.load().alaya_exch_free(b)
 
 
-@pytest.mark.parametrize("world,lens", [(2, (6000, 7000)), (3, (2, 9000)), (4, (5000, 1))])
-def test_fused_sharded_step_emulated(cuda_ok, world, lens):
+@pytest.mark.parametrize("world,lens,beta", [(2, (6000, 7000), 5.0), (3, (2, 9000), 5.0), (4, (5000, 1), 5.0),
+                                             (3, (7000, 9000), 140.0)])
+def test_fused_sharded_step_emulated(cuda_ok, world, lens, beta):
     """alaya_sharded_step (scan -> per-group max over peer memory -> attend) for
     2-4 ranks emulated on streams of one GPU at a size whose grids co-reside
     (each rank's attend waits on the others' scans: the bounded poll turns a
     missed arrival into the error flag, not a hang), vs the unsharded kernels.
     Sequences shorter than the world leave shards with no tokens of them: those
-    ranks export -inf maxima from prep_kernel."""
+    ranks export -inf maxima from prep_kernel. beta = 140 runs the group candidate
+    format (attend_grp_kernel reading the ranks' pushed maxima)."""
     from paper_2504_10326_b200 import _lib, engine
     from paper_2504_10326_b200.sharded import EngineStages, local_view
     dev = torch.device("cuda")
-    B, hkv, g, d, w, beta = len(lens), 2, 4, 128, 3, 5.0
+    B, hkv, g, d, w = len(lens), 2, 4, 128, 3
     dtype = torch.bfloat16
     r = np.random.default_rng(9 + world)
     K, V, WK, WV, qs = [], [], [], [], []
