@@ -289,7 +289,12 @@ template <typename T, int D, int G, bool L2>
 __device__ __forceinline__ void sel_task_pipe(const Batch& bt, const float* __restrict__ smax_ext,
                                               const Ws& ws, size_t cj, int qb, int qe, int lane,
                                               int (*s_t)[32], float (*s_w)[32], bool want_values) {
-  constexpr int DPL = D / 16, U = kGatherU;
+  // rows in flight per half-warp: one 32-candidate batch in one round when a lane's
+  // share of a row is <= 16 B (bf16 d=128), else in 2+ rounds of fewer rows (fp32 rows
+  // are 32 B per lane: 16 of them would need 128 registers and spill)
+  constexpr int DPL = D / 16;
+  constexpr int U = (int)sizeof(T) * DPL <= 16 ? kGatherU : kGatherU * 16 / ((int)sizeof(T) * DPL);
+  constexpr int ROUNDS = kGatherU / U;
   const int hl = lane & 15, half = lane >> 4;
   // sub-lists [qb, qe) of pair cj = (chunk c, head j) as one virtual list; the
   // primary task (qb = 0) writes slot cj, an overflow task (qb > 0) slot cj*4+qb
@@ -360,26 +365,30 @@ __device__ __forceinline__ void sel_task_pipe(const Batch& bt, const float* __re
       cur ^= 1;
       continue;
     }
-    RawFrag<T, DPL> f[U];
-    float wk[U];
+    int ns_nxt = 0;
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int r = 2 * k + half;
-      if (r < ns_cur) {
-        f[k].load(vb + (size_t)s_t[cur][r] * D);
-        wk[k] = s_w[cur][r];
-      } else {
-        f[k].zero();
-        wk[k] = 0.f;
+    for (int rd = 0; rd < ROUNDS; ++rd) {
+      RawFrag<T, DPL> f[U];
+      float wk[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int r = 2 * (rd * U + k) + half;
+        if (r < ns_cur) {
+          f[k].load(vb + (size_t)s_t[cur][r] * D);
+          wk[k] = s_w[cur][r];
+        } else {
+          f[k].zero();
+          wk[k] = 0.f;
+        }
       }
-    }
-    const int ns_nxt = more ? filter(cur ^ 1) : 0;  // overlaps the loads above
+      if (rd == 0) ns_nxt = more ? filter(cur ^ 1) : 0;  // overlaps the loads above
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      float x[DPL];
-      f[k].to_float(x);
+      for (int k = 0; k < U; ++k) {
+        float x[DPL];
+        f[k].to_float(x);
 #pragma unroll
-      for (int e = 0; e < DPL; ++e) acc[e] = fmaf(wk[k], x[e], acc[e]);
+        for (int e = 0; e < DPL; ++e) acc[e] = fmaf(wk[k], x[e], acc[e]);
+      }
     }
     if (!more) break;
     cur ^= 1;

@@ -173,9 +173,10 @@ bool gfmt_enabled(const Batch& bt) {
 }
 
 // CUDA-core scan (fp32 K/V, other dims) with the attend beside it: persistent scan
-// grid (ALAYA_OVERLAP_CC=0: one CTA per chunk, the attend after the scan)
+// grid (ALAYA_OVERLAP_CC=1; default off: one CTA per chunk, the attend after the
+// scan -- fp32 128K B=4 490 vs 542 us, B=1 165 vs 162 us, profiles/r02/fp32_attend_rounds_v54.jsonl)
 bool cc_overlap_enabled() {
-  static const int on = env_int("ALAYA_OVERLAP_CC", 1);
+  static const int on = env_int("ALAYA_OVERLAP_CC", 0);
   return on != 0;
 }
 int persist_less(const Batch& bt) {
