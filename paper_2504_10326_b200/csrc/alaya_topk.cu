@@ -496,7 +496,9 @@ __global__ void __launch_bounds__(kSelThreads)
   const int nb = bi.n_blocks, r = bi.r;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int hl = lane & 15, hw = threadIdx.x >> 4;  // half-warp per representative row
-  constexpr int DPL = D / 16, U = 16, NHW = kSelThreads / 16;
+  // representative rows in flight per half-warp: 16, or 8 when a lane's share of a
+  // row is 32 B (fp32 d = 128; 16 would need 128 registers and spill)
+  constexpr int DPL = D / 16, U = (int)sizeof(T) * DPL <= 16 ? 16 : 8, NHW = kSelThreads / 16;
   float qr[DPL];
   load_q<DPL>(q + (size_t)row * D + hl * DPL, qr);
   for (int i = threadIdx.x; i < nb; i += blockDim.x) s_score[i] = 0u;  // -inf
@@ -594,6 +596,9 @@ __global__ void __launch_bounds__(kSaWarps * 32)
                        const int32_t* __restrict__ count, float* __restrict__ out,
                        int32_t* __restrict__ nsel_out, int* __restrict__ status) {
   constexpr int DPL = D / 16;
+  // K and V rows of a batch in flight: 8 per half-warp, 4 when a lane's share of a
+  // row is 32 B (fp32 d = 128: 8 x 2 x 32 B would need 128 registers and spill)
+  constexpr int U = (int)sizeof(T) * DPL <= 16 ? kSaU : kSaU / 2;
   __shared__ float s_m[kSaWarps], s_l[kSaWarps];
   __shared__ float s_acc[kSaWarps][D];
   __shared__ int s_sel[kSaWarps];
@@ -619,11 +624,11 @@ __global__ void __launch_bounds__(kSaWarps * 32)
   const T* vbase = reinterpret_cast<const T*>(s.v) + (size_t)h * s.hs;
   const T* wkb = reinterpret_cast<const T*>(s.wk) + (size_t)h * s.whs;
   const T* wvb = reinterpret_cast<const T*>(s.wv) + (size_t)h * s.whs;
-  constexpr int STEP = 2 * kSaU;  // rows per warp per iteration
+  constexpr int STEP = 2 * U;  // rows per warp per iteration
   // the ids of a warp's next rows are loaded one iteration ahead
-  auto load_ids = [&](int r0, int64_t (&g)[kSaU]) {
+  auto load_ids = [&](int r0, int64_t (&g)[U]) {
 #pragma unroll
-    for (int u = 0; u < kSaU; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int r = r0 + 2 * u + half;
       g[u] = r < nid ? __ldg(rid + r) : -1;
     }
@@ -653,31 +658,31 @@ __global__ void __launch_bounds__(kSaWarps * 32)
 #pragma unroll
   for (int e = 0; e < DPL; ++e) acc[e] = 0.f;
   int nsel = 0;
-  int64_t gcur[kSaU], gnxt[kSaU];
+  int64_t gcur[U], gnxt[U];
   int r0 = warp * STEP;
   load_ids(r0, gcur);
   for (; r0 < R; r0 += kSaWarps * STEP) {
     load_ids(r0 + kSaWarps * STEP, gnxt);
-    const T* kr[kSaU];
-    const T* vr[kSaU];
+    const T* kr[U];
+    const T* vr[U];
 #pragma unroll
-    for (int u = 0; u < kSaU; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int r = r0 + 2 * u + half;
       rows_of(r, gcur[u], kr[u], vr[u]);
       if (hl == 0 && r < nid && kr[u]) ++nsel;  // lanes 0 and 16 count their rows
     }
-    float z[kSaU];
-    RawFrag<T, DPL> fk[kSaU], fv[kSaU];
+    float z[U];
+    RawFrag<T, DPL> fk[U], fv[U];
 #pragma unroll
-    for (int u = 0; u < kSaU; ++u) {
+    for (int u = 0; u < U; ++u) {
       if (kr[u]) { fk[u].load(kr[u] + hl * DPL); fv[u].load(vr[u] + hl * DPL); }
       else { fk[u].zero(); fv[u].zero(); }
     }
 #pragma unroll
-    for (int u = 0; u < kSaU; ++u) gcur[u] = gnxt[u];
+    for (int u = 0; u < U; ++u) gcur[u] = gnxt[u];
     float bm = -INFINITY;
 #pragma unroll
-    for (int u = 0; u < kSaU; ++u) {
+    for (int u = 0; u < U; ++u) {
       float x[DPL];
       fk[u].to_float(x);
       float a = 0.f;
@@ -696,7 +701,7 @@ __global__ void __launch_bounds__(kSaWarps * 32)
 #pragma unroll
     for (int e = 0; e < DPL; ++e) acc[e] *= sc;
 #pragma unroll
-    for (int u = 0; u < kSaU; ++u) {
+    for (int u = 0; u < U; ++u) {
       const float w = kr[u] ? expf(z[u] - mn) : 0.f;
       lb += w;
       float x[DPL];
