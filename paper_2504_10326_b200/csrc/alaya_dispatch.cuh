@@ -94,7 +94,8 @@ struct Stages {
       if (per_sm < 1) per_sm = 1;
     }
     const long tasks = (long)bt.total_chunks * G + (bt.win_in_prep ? 0 : (long)bt.B * bt.Hq);
-    const long blocks = std::min<long>((tasks + 3) / 4, (long)per_sm * num_sms());
+    constexpr int kW = kOvlThreads / 32;
+    const long blocks = std::min<long>((tasks + kW - 1) / kW, (long)per_sm * num_sms());
     if (blocks == 0) return ALAYA_OK;  // (no base chunks, window partials from prep)
     return launch_pdl("attend_ovl_kernel", attend_ovl_kernel<T, D, G>, (unsigned)blocks, kOvlThreads, 0,
                       st, bt, q, ws);

@@ -567,10 +567,15 @@ __device__ __forceinline__ void sx_global_max(const Batch& bt, const Ws& ws, int
 // every epilogue warp of every chunk of the group has published (the group's
 // max is final); heavy pairs' overflow items wait for the whole scan. Window
 // tasks need nothing from the scan and go first.
-constexpr int kOvlThreads = 128;
+// 2-warp CTAs: finer-grained residency beside the scan CTAs (B=4 layer 221 -> 219 us,
+// B=8 429 -> 426.5 vs 4-warp CTAs, profiles/r02/ovl64_v63.jsonl)
+#ifndef ALAYA_OVL_THREADS
+#define ALAYA_OVL_THREADS 64
+#endif
+constexpr int kOvlThreads = ALAYA_OVL_THREADS;
 
 template <typename T, int D, int G>
-__global__ void __launch_bounds__(kOvlThreads, 4)  // <= 128 regs: one CTA fits beside 3 scan CTAs
+__global__ void __launch_bounds__(kOvlThreads, 512 / kOvlThreads)  // <= 128 regs
     attend_ovl_kernel(const __grid_constant__ Batch bt, const float* __restrict__ q, Ws ws) {
   constexpr int W = kOvlThreads / 32;
   __shared__ int s_t[W][2][32];
@@ -858,6 +863,17 @@ __global__ void __launch_bounds__(CW * 32)
   const int h = qh / G, j = qh - h * G;
   const KSeq& s = bt.s[b];
   const int c0 = s.chunk_base + h * s.nch;
+  // warp 0's epilogue inputs (max, window partial) are loaded up front, in flight
+  // with the chunk partials instead of a dependent round trip after the reduction
+  float smax = 0.f, mw = 0.f, lw = 0.f, wpe[DL];
+  const float* wp = ws.partbuf + (size_t)row * (D + 2);
+  if (warp == 0) {
+    smax = smax_ext ? smax_ext[row] : dec_max(ws.gmax[row]);
+    mw = wp[0];
+    lw = wp[1];
+#pragma unroll
+    for (int k = 0; k < DL; ++k) wpe[k] = lane + 32 * k < D ? wp[2 + lane + 32 * k] : 0.f;
+  }
   float ab[DL];
 #pragma unroll
   for (int k = 0; k < DL; ++k) ab[k] = 0.f;
@@ -914,11 +930,8 @@ __global__ void __launch_bounds__(CW * 32)
 #pragma unroll
   for (int w = 0; w < CW; ++w) { lb += redl[w]; nsel += redn[w]; }
   if (nsel == 0) lb = 0.f;
-  const float smax = smax_ext ? smax_ext[row] : dec_max(ws.gmax[row]);
   if (smax_out && lane == 0) smax_out[row] = smax;
   const float zmax = smax * bt.inv_sqrt_d;
-  const float* wp = ws.partbuf + (size_t)row * (D + 2);
-  const float mw = wp[0], lw = wp[1];
   const bool hb = lb > 0.f, hwn = lw > 0.f;
   const float m = fmaxf(hb ? zmax : -INFINITY, hwn ? mw : -INFINITY);
   const float fb = hb ? expf(zmax - m) : 0.f;
@@ -932,7 +945,7 @@ __global__ void __launch_bounds__(CW * 32)
     float sb = 0.f;
 #pragma unroll
     for (int w = 0; w < CW; ++w) sb += red[w][e];
-    const float a = sb * fb + (hwn ? wp[2 + e] * fw : 0.f);
+    const float a = sb * fb + (hwn ? wpe[k] * fw : 0.f);
     if (out) {
       const float o = a / l;
       if (!isfinite(o)) atomicExch(ws.status, (int)ALAYA_ERR_NONFINITE);

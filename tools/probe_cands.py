@@ -4,7 +4,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2504_10326_b200 import engine
 dev = torch.device("cuda")
-B, Hkv, n, d, Hq = 4, 8, 131072, 128, 32
+B, Hkv, n, d, Hq = int(os.environ.get("B", "4")), 8, 131072, 128, 32
+CH = 2048 if B >= 4 else 1024  # the auto chunk at 128K
 g = torch.Generator(device=dev).manual_seed(0)
 c = torch.randn(16, d, generator=g, device=dev); c = c / c.norm(dim=1, keepdim=True) * math.sqrt(d)
 K = torch.empty(B, Hkv, n, d, dtype=torch.bfloat16, device=dev)
@@ -17,8 +18,8 @@ for scan in (2, 1):
     call = engine.Call([engine.SeqView(k=K[b], v=K[b], n=n) for b in range(B)], p, torch.bfloat16, dev)
     call.dipr_attention(q)
     torch.cuda.synchronize()
-    cnt = call.candidate_counts(2048).sum(-1).float()
+    cnt = call.candidate_counts(CH).sum(-1).float()
     ids, nsel, _ = call.selected(n)
-    print(json.dumps({"scan": scan, "pairs": cnt.numel(), "mean": cnt.mean().item(), "max": cnt.max().item(),
+    print(json.dumps({"B": B, "chunk": CH, "scan": scan, "pairs": cnt.numel(), "mean": cnt.mean().item(), "max": cnt.max().item(),
                       "p99": cnt.quantile(0.99).item(), "gt512": int((cnt > 512).sum()),
                       "selected_mean_per_head": nsel.float().mean().item()}))
