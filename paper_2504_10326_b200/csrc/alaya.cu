@@ -419,8 +419,11 @@ int dipr_attention_impl(const alaya_params* p, const alaya_seq* seqs, int batch,
     c.bt.overlap = 1;
     c.bt.gfmt = gfmt_enabled(c.bt);
     if ((rc = run_scan(c, d_q))) return rc;
-    if ((rc = c.bt.gfmt ? c.st.attend_grp(c.bt, d_q, c.ws, c.stream) : c.st.attend_ovl(c.bt, d_q, c.ws, c.stream)))
-      return rc;
+    if (c.bt.gfmt && dense_attend_enabled(c.bt, c.seqs))
+      rc = launch_tc_attend_dense(c.bt, c.seqs, c.ws, c.stream);
+    else
+      rc = c.bt.gfmt ? c.st.attend_grp(c.bt, d_q, c.ws, c.stream) : c.st.attend_ovl(c.bt, d_q, c.ws, c.stream);
+    if (rc) return rc;
     return c.st.combine(c.bt, nullptr, c.ws, d_out, nullptr, c.ws.smaxbuf, c.stream);
   }
   if (!c.use_tc && cc_overlap_enabled()) {  // CUDA-core scan: persistent, attend beside it

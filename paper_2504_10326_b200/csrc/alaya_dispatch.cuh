@@ -178,6 +178,8 @@ StageSet pick_g(int G) {
 bool tc_scan_eligible(const Batch& bt, int dtype, const alaya_seq* seqs);
 int launch_tc_scan(const Batch& bt, const alaya_seq* seqs, const float* q, const Ws& ws,
                    cudaStream_t st);
+bool dense_attend_enabled(const Batch& bt, const alaya_seq* seqs);
+int launch_tc_attend_dense(const Batch& bt, const alaya_seq* seqs, const Ws& ws, cudaStream_t st);
 bool overlap_enabled();
 bool gfmt_enabled(const Batch& bt);
 bool cc_overlap_enabled();

@@ -9,6 +9,7 @@
 
 #include "alaya_dispatch.cuh"
 #include "alaya_tc.cuh"
+#include "alaya_tc_attend.cuh"
 
 namespace alaya {
 
@@ -94,8 +95,8 @@ int launch(const Batch& bt, const tc::Maps& maps, const float* q, const Ws& ws, 
   return launch_s<G, 6>(bt, maps, q, ws, st, 1);
 }
 
-// One TMA tensor map per distinct K slab (sessions sharing a context share it).
-int build_maps(const Batch& bt, const alaya_seq* seqs, tc::Maps& maps) {
+// One TMA tensor map per distinct K (or V: use_v) slab (sessions sharing a context share it).
+int build_maps(const Batch& bt, const alaya_seq* seqs, tc::Maps& maps, bool use_v = false) {
   auto enc = encode_fn();
   // L2 sector promotion of the K boxes: ALAYA_TC_PROMO 0..3 = none/64B/128B/256B
   static const CUtensorMapL2promotion promo =
@@ -107,7 +108,7 @@ int build_maps(const Batch& bt, const alaya_seq* seqs, tc::Maps& maps) {
     if (seqs[b].n == 0) continue;
     int found = -1;
     for (int a = 0; a < b && found < 0; ++a)
-      if (seqs[a].n && seqs[a].k == seqs[b].k) found = maps.map_of_seq[a];
+      if (seqs[a].n && (use_v ? seqs[a].v == seqs[b].v : seqs[a].k == seqs[b].k)) found = maps.map_of_seq[a];
     if (found >= 0) { maps.map_of_seq[b] = (int16_t)found; continue; }
     const cuuint64_t rows = (cuuint64_t)bt.Hkv * (seqs[b].head_stride / 128);
     // encoded maps are cached per (slab, rows): decode steps re-use the same slabs
@@ -115,8 +116,9 @@ int build_maps(const Batch& bt, const alaya_seq* seqs, tc::Maps& maps) {
     static thread_local Cached cache[64];
     static thread_local int cache_next = 0;
     const Cached* hit = nullptr;
+    const void* slab = use_v ? seqs[b].v : seqs[b].k;
     for (int i = 0; i < 64 && !hit; ++i)
-      if (cache[i].k == seqs[b].k && cache[i].rows == rows) hit = &cache[i];
+      if (cache[i].k == slab && cache[i].rows == rows) hit = &cache[i];
     if (hit) {
       maps.m[nmaps] = hit->m;
       maps.map_of_seq[b] = (int16_t)nmaps++;
@@ -126,18 +128,66 @@ int build_maps(const Batch& bt, const alaya_seq* seqs, tc::Maps& maps) {
     cuuint64_t gstride[1] = {256};
     cuuint32_t box[2] = {64, (cuuint32_t)tc::kTileKeys};
     cuuint32_t estride[2] = {1, 1};
-    CUresult r = enc(&maps.m[nmaps], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(seqs[b].k),
+    CUresult r = enc(&maps.m[nmaps], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(slab),
                      gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_128B, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(ALAYA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-    cache[cache_next] = {seqs[b].k, rows, maps.m[nmaps]};
+    cache[cache_next] = {slab, rows, maps.m[nmaps]};
     cache_next = (cache_next + 1) % 64;
     maps.map_of_seq[b] = (int16_t)nmaps++;
   }
   return ALAYA_OK;
 }
 
+template <int G>
+int launch_dense(const Batch& bt, const tc::Maps& vmaps, const Ws& ws, cudaStream_t st) {
+  const size_t sm = tc::dense_smem_bytes(G);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tc::attend_dense_tc_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  return launch_pdl("attend_dense_tc_kernel", tc::attend_dense_tc_kernel<G>, bt.total_chunks, tc::kThreadsDense,
+                    sm, st, bt, vmaps, ws);
+}
+
 }  // namespace
+
+// Dense tensor-core group attend (alaya_tc_attend.cuh) for every group-format call
+// (beta / sqrt(d) >= 11.5: the heads keep most rows of a chunk), bf16 V slabs laid
+// out like K (TMA-able), not in the fused sharded step. ALAYA_GRP_DENSE=0 keeps the
+// gather kernel (attend_grp_kernel). Measured at beta = 140 (profiles/r02/dense_attend_v66.jsonl):
+// Llama B=1 126 -> 117 us, B=4 446 -> 431, Qwen 40/8 B=1 139 -> 124, B=8 902 -> 910.
+bool dense_attend_enabled(const Batch& bt, const alaya_seq* seqs) {
+  static const int mode = env_int("ALAYA_GRP_DENSE", 1);
+  if (!mode || !bt.gfmt || bt.sx_on || bt.D != 128) return false;
+  int distinct = 0;
+  for (int b = 0; b < bt.B; ++b) {
+    if (seqs[b].n == 0) continue;
+    if (seqs[b].head_stride % 128 || reinterpret_cast<uintptr_t>(seqs[b].v) % 16) return false;
+    bool seen = false;
+    for (int a = 0; a < b && !seen; ++a) seen = seqs[a].v == seqs[b].v;
+    distinct += !seen;
+  }
+  return distinct <= tc::kMaxMaps;
+}
+
+int launch_tc_attend_dense(const Batch& bt, const alaya_seq* seqs, const Ws& ws, cudaStream_t st) {
+  if (bt.total_chunks == 0) return ALAYA_OK;
+  static thread_local tc::Maps vmaps;
+  int rc = build_maps(bt, seqs, vmaps, true);
+  if (rc) return rc;
+  switch (bt.G) {
+    case 1: return launch_dense<1>(bt, vmaps, ws, st);
+    case 2: return launch_dense<2>(bt, vmaps, ws, st);
+    case 3: return launch_dense<3>(bt, vmaps, ws, st);
+    case 4: return launch_dense<4>(bt, vmaps, ws, st);
+    case 5: return launch_dense<5>(bt, vmaps, ws, st);
+    case 6: return launch_dense<6>(bt, vmaps, ws, st);
+    case 7: return launch_dense<7>(bt, vmaps, ws, st);
+    default: return launch_dense<8>(bt, vmaps, ws, st);
+  }
+}
 
 bool tc_scan_eligible(const Batch& bt, int dtype, const alaya_seq* seqs) {
   if (dtype != ALAYA_BF16 || bt.D != 128 || bt.G > 8 || bt.chunk % (4 * tc::kTileKeys)) return false;
