@@ -3,11 +3,13 @@
 // dipr.py:64 filter, store.py:271-278 selection, attention.py:98-110 partial).
 //
 // One CTA per chunk. The chunk's V rows stream densely through a TMA ring (the
-// same 32 KB SW128 tiles as the K scan); per 128-row tile the 4 builder warps
-// (one per lane quarter, matching the scan's group-format sub-lists) apply every
+// same 32 KB SW128 tiles as the K scan); per 128-row tile the 8 builder warps
+// (two per lane quarter, matching the scan's group-format sub-lists) apply every
 // head's exact filter s_j >= gmax_j - beta minus the window ids to the tile's
 // listed rows and write the weights w_j = 2^((s_j - gmax_j) log2e / sqrt(d)) as
-// the B operand (3 bf16 terms per weight, zeros for unlisted rows):
+// the B operand (3 bf16 terms per weight, zeros for unlisted rows; two warps per
+// quarter, each for half of the heads: one warp per quarter was builder-bound,
+// 274 vs 249 us for the kernel alone at beta 140 B=4):
 //   D[d][n] += V^T[d][t] * W[t][n],  M = 128 (d), N = 3G padded, K = 16 tokens,
 // A = the V tile read MN-major (d contiguous), fp32 accumulation in TMEM over the
 // whole chunk. A row any head keeps is read once, by a stream instead of a
@@ -22,7 +24,8 @@ namespace alaya {
 namespace tc {
 
 constexpr int kDenseStages = 3;
-constexpr int kThreadsDense = 192;  // TMA producer, MMA issuer, 4 builder/epilogue warps
+constexpr int kThreadsDense = 320;  // TMA producer, MMA issuer, 8 builder/epilogue warps
+// (two per lane quarter, each for half of the GQA group's heads)
 
 // MN-major, 128B-swizzled UMMA descriptor of a V tile read as A = V^T (M = d):
 // 64 d (128 B) contiguous, the next 64 d one box (16 KB) away (LBO); 8 token
@@ -38,7 +41,7 @@ inline size_t dense_smem_bytes(int G) {
 }
 
 template <int G>
-__global__ void __launch_bounds__(kThreadsDense, 2)
+__global__ void __launch_bounds__(kThreadsDense, 2)  // <= 102 registers
     attend_dense_tc_kernel(const __grid_constant__ Batch bt, const __grid_constant__ Maps vmaps, Ws ws) {
   constexpr int NP = (3 * G <= 16) ? 16 : 32;
   constexpr int kBBytes = 2 * NP * 128;  // B operand: NP rows x 128 tokens, two 64-token boxes
@@ -69,7 +72,7 @@ __global__ void __launch_bounds__(kThreadsDense, 2)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kDenseStages; ++i) { mbar_init(full_bar(i), 1); mbar_init(empty_bar(i), 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(bfull0 + 8u * i, 4); mbar_init(bfree0 + 8u * i, 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(bfull0 + 8u * i, 8); mbar_init(bfree0 + 8u * i, 1); }
     mbar_init(accf, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -139,8 +142,10 @@ __global__ void __launch_bounds__(kThreadsDense, 2)
       if (++stage == kDenseStages) { stage = 0; phase ^= 1; }
     }
   } else {
-    // ===================== builders / epilogue (lane quarter q) =====================
-    const int quarter = warp & 3;
+    // ===================== builders / epilogue (lane quarter q, heads of half hf) =====================
+    constexpr int GH = (G + 1) / 2;  // heads per builder warp
+    const int quarter = warp & 3, hf = (warp - 2) >> 2;
+    const int jb = hf * GH;  // this warp's heads: jb + jj < G, jj < GH
     const float k2 = bt.inv_sqrt_d * kLog2e;
     if (lane == 0) {
       const int* gd = ws.group_done + b * bt.Hkv + h;
@@ -151,38 +156,50 @@ __global__ void __launch_bounds__(kThreadsDense, 2)
     // batches of the list in one round trip (entries past the length are masked
     // later; the list region holds qcap entries)
     constexpr int kPF = 3;  // list batches in registers: the current one + 2 ahead
-    float gm[G], th[G], lsum[G];
-    int nsel[G], nret[G];
+    float gm[GH], th[GH], lsum[GH];
+    int nsel[GH], nret[GH];
     const int* gi = ws.gidx + (size_t)c * chunk + quarter * qcap;
     const float* gs = ws.cscore + (size_t)(c * 4 + quarter) * G * qcap;
     const int n = __ldcg(&ws.cnt[(size_t)c * 4 + quarter]);
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      gm[j] = dec_max(__ldcg(&ws.gmax[b * bt.Hq + h * G + j]));
-      lsum[j] = 0.f;
-      nsel[j] = nret[j] = 0;
+    for (int jj = 0; jj < GH; ++jj) {
+      const int j = jb + jj;
+      gm[jj] = j < G ? dec_max(__ldcg(&ws.gmax[b * bt.Hq + h * G + j])) : 0.f;
+      lsum[jj] = 0.f;
+      nsel[jj] = nret[jj] = 0;
     }
     int row_q[kPF];
-    float sc_q[kPF][G];
+    float sc_q[kPF][GH];
 #pragma unroll
     for (int p = 0; p < kPF; ++p) {
       const int ii = p * 32 + lane;
       row_q[p] = ii < qcap ? __ldcg(gi + ii) : 0;
 #pragma unroll
-      for (int j = 0; j < G; ++j) sc_q[p][j] = ii < qcap ? __ldcg(gs + j * qcap + ii) : -INFINITY;
+      for (int jj = 0; jj < GH; ++jj)
+        sc_q[p][jj] = (ii < qcap && jb + jj < G) ? __ldcg(gs + (jb + jj) * qcap + ii) : -INFINITY;
     }
 #pragma unroll
-    for (int j = 0; j < G; ++j) th[j] = gm[j] - bt.beta;
+    for (int jj = 0; jj < GH; ++jj) th[jj] = gm[jj] - bt.beta;
     int i0 = 0;
-    const int box = quarter >> 1, c16_0 = (quarter & 1) * 4;  // this warp's 32 token columns of B
+    const int box = quarter >> 1, c16_0 = (quarter & 1) * 4;  // this quarter's 32 token columns of B
+    // B rows this warp owns: sp*G + j for its heads (half 0 also the padding rows 3G..NP-1)
+    const int nrows_own = 3 * GH + (hf == 0 ? NP - 3 * G : 0);
+    auto own_row = [&](int r) {  // r < nrows_own
+      if (r < 3 * GH) {
+        const int sp = r / GH, jj = r - sp * GH;
+        return jb + jj < G ? sp * G + jb + jj : -1;
+      }
+      return 3 * G + (r - 3 * GH);
+    };
     for (int tl = 0; tl < ntiles; ++tl) {
       const int bi = tl & 1;
       if (tl >= 2) mbar_wait(bfree0 + 8u * bi, (uint32_t)((tl >> 1) - 1) & 1u);
       uint8_t* bb = bbuf + bi * kBBytes;
-      for (int i = lane; i < NP * 4; i += 32) {  // zero this warp's columns of every B row
-        const int nn = i >> 2, c16 = c16_0 + (i & 3);
-        *reinterpret_cast<uint4*>(bb + box * (NP * 128) + (nn >> 3) * 1024 + (nn & 7) * 128 +
-                                  ((c16 ^ (nn & 7)) << 4)) = make_uint4(0, 0, 0, 0);
+      for (int i = lane; i < nrows_own * 4; i += 32) {  // zero this warp's rows in its quarter's columns
+        const int nn = own_row(i >> 2), c16 = c16_0 + (i & 3);
+        if (nn >= 0)
+          *reinterpret_cast<uint4*>(bb + box * (NP * 128) + (nn >> 3) * 1024 + (nn & 7) * 128 +
+                                    ((c16 ^ (nn & 7)) << 4)) = make_uint4(0, 0, 0, 0);
       }
       __syncwarp();
       // listed rows of this tile (the sub-list is in token order; a batch may span tiles)
@@ -193,16 +210,18 @@ __global__ void __launch_bounds__(kThreadsDense, 2)
         const bool inwin = mine && in_window(s.off + t0 + row_q[0], s.P, bt.wi, bt.wl);
         const int k = row_q[0] & 127, kk = k & 63, c16 = kk >> 3, wpos = kk & 7;
 #pragma unroll
-        for (int j = 0; j < G; ++j) {
-          const bool pass = mine && sc_q[0][j] >= th[j];
+        for (int jj = 0; jj < GH; ++jj) {
+          const int j = jb + jj;
+          if (j >= G) break;  // (warp-uniform)
+          const bool pass = mine && sc_q[0][jj] >= th[jj];
           const bool sel = pass && !inwin;
-          const unsigned bs = __ballot_sync(kFull, sel), br = __ballot_sync(kFull, pass);
+          const unsigned bs = __ballot_sync(kFull, sel);
           if (sel)  // selected ids of (chunk, head j), quarter list (diagnostics)
-            ws.cidx[((size_t)c * G + j) * chunk + quarter * qcap + nsel[j] + __popc(bs & lanemask_lt())] = row_q[0];
-          nsel[j] += __popc(bs);
-          nret[j] += __popc(br);
-          const float w = sel ? exp2f((sc_q[0][j] - gm[j]) * k2) : 0.f;
-          lsum[j] += w;
+            ws.cidx[((size_t)c * G + j) * chunk + quarter * qcap + nsel[jj] + __popc(bs & lanemask_lt())] = row_q[0];
+          nsel[jj] += __popc(bs);
+          nret[jj] += pass ? 1 : 0;  // per lane, summed at the end
+          const float w = sel ? exp2f((sc_q[0][jj] - gm[jj]) * k2) : 0.f;
+          lsum[jj] += w;
           if (mine) {
             const __nv_bfloat16 hi = __float2bfloat16_rn(w);
             const float r1 = w - __bfloat162float(hi);
@@ -223,38 +242,39 @@ __global__ void __launch_bounds__(kThreadsDense, 2)
         for (int p = 0; p + 1 < kPF; ++p) {
           row_q[p] = row_q[p + 1];
 #pragma unroll
-          for (int j = 0; j < G; ++j) sc_q[p][j] = sc_q[p + 1][j];
+          for (int jj = 0; jj < GH; ++jj) sc_q[p][jj] = sc_q[p + 1][jj];
         }
         const int ii = i0 + (kPF - 1) * 32 + lane;
         row_q[kPF - 1] = ii < n ? __ldcg(gi + ii) : 0;
 #pragma unroll
-        for (int j = 0; j < G; ++j) sc_q[kPF - 1][j] = ii < n ? __ldcg(gs + j * qcap + ii) : -INFINITY;
+        for (int jj = 0; jj < GH; ++jj)
+          sc_q[kPF - 1][jj] = (ii < n && jb + jj < G) ? __ldcg(gs + (jb + jj) * qcap + ii) : -INFINITY;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tcgen05 reads
       __syncwarp();
       if (lane == 0) mbar_arrive(bfull0 + 8u * bi);
     }
     // epilogue: lane = d, columns sp*G + j -> the (chunk, head j) partial
-    if (ntiles > 0) {
-      mbar_wait(accf, 0);
-      fence_after();
-    }
+    mbar_wait(accf, 0);
+    fence_after();
     float v[NP];
-    if (ntiles > 0) {
-      tmem_ld<NP>(tmem + ((uint32_t)(quarter * 32) << 16), v);
-    } else {
-#pragma unroll
-      for (int i = 0; i < NP; ++i) v[i] = 0.f;
-    }
+    tmem_ld<NP>(tmem + ((uint32_t)(quarter * 32) << 16), v);
     const size_t cj0 = (size_t)c * G;
     const int d = quarter * 32 + lane;
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      ws.part_acc[(cj0 + j) * D + d] = (v[j] + v[G + j]) + v[2 * G + j];
-      const float l = warp_sum(lsum[j]);
-      if (lane == 0) { s_l[quarter][j] = l; s_ns[quarter][j] = nsel[j]; s_nr[quarter][j] = nret[j]; }
+    for (int jj = 0; jj < GH; ++jj) {
+      const int j = jb + jj;
+      if (j >= G) break;
+      float o = 0.f;
+#pragma unroll
+      for (int jx = 0; jx < G; ++jx)  // (register-indexed v: select the head's columns)
+        if (jx == j) o = (v[jx] + v[G + jx]) + v[2 * G + jx];
+      ws.part_acc[(cj0 + j) * D + d] = o;
+      const float l = warp_sum(lsum[jj]);
+      const int nr = (int)warp_sum((float)nret[jj]);
+      if (lane == 0) { s_l[quarter][j] = l; s_ns[quarter][j] = nsel[jj]; s_nr[quarter][j] = nr; }
     }
-    asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 builder warps
+    asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 builder warps
     if (warp == 2 && lane < G) {
       const int j = lane;
       float l = 0.f;

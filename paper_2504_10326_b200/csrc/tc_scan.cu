@@ -156,8 +156,10 @@ int launch_dense(const Batch& bt, const tc::Maps& vmaps, const Ws& ws, cudaStrea
 // Dense tensor-core group attend (alaya_tc_attend.cuh) for every group-format call
 // (beta / sqrt(d) >= 11.5: the heads keep most rows of a chunk), bf16 V slabs laid
 // out like K (TMA-able), not in the fused sharded step. ALAYA_GRP_DENSE=0 keeps the
-// gather kernel (attend_grp_kernel). Measured at beta = 140 (profiles/r02/dense_attend_v66.jsonl):
-// Llama B=1 126 -> 117 us, B=4 446 -> 431, Qwen 40/8 B=1 139 -> 124, B=8 902 -> 910.
+// gather kernel (attend_grp_kernel). Measured at beta = 140 (profiles/r02/dense_headsplit_v69.jsonl):
+// Llama B=1 126 -> 115 us, B=4 446 -> 409, B=8 843 -> 821, Qwen 40/8 B=1 139 -> 126, B=8 902 -> 894;
+// at beta = 130 the per-head attend stays ahead (B=8 729 vs 802), so the group-format
+// threshold is unchanged.
 bool dense_attend_enabled(const Batch& bt, const alaya_seq* seqs) {
   static const int mode = env_int("ALAYA_GRP_DENSE", 1);
   if (!mode || !bt.gfmt || bt.sx_on || bt.D != 128) return false;
