@@ -3,13 +3,13 @@
 // dipr.py:64 filter, store.py:271-278 selection, attention.py:98-110 partial).
 //
 // One CTA per chunk. The chunk's V rows stream densely through a TMA ring (the
-// same 32 KB SW128 tiles as the K scan); per 128-row tile the 8 builder warps
-// (two per lane quarter, matching the scan's group-format sub-lists) apply every
+// same 32 KB SW128 tiles as the K scan); per 128-row tile the builder warps
+// (2-4 per lane quarter, matching the scan's group-format sub-lists) apply every
 // head's exact filter s_j >= gmax_j - beta minus the window ids to the tile's
 // listed rows and write the weights w_j = 2^((s_j - gmax_j) log2e / sqrt(d)) as
-// the B operand (3 bf16 terms per weight, zeros for unlisted rows; two warps per
-// quarter, each for half of the heads: one warp per quarter was builder-bound,
-// 274 vs 249 us for the kernel alone at beta 140 B=4):
+// the B operand (3 bf16 terms per weight, zeros for unlisted rows; 2-4 warps per
+// quarter, each for a share of the heads: one warp per quarter was builder-bound,
+// 274 vs 249 us for the kernel alone at beta 140 B=4 with two):
 //   D[d][n] += V^T[d][t] * W[t][n],  M = 128 (d), N = 3G padded, K = 16 tokens,
 // A = the V tile read MN-major (d contiguous), fp32 accumulation in TMEM over the
 // whole chunk. A row any head keeps is read once, by a stream instead of a
@@ -24,8 +24,12 @@ namespace alaya {
 namespace tc {
 
 constexpr int kDenseStages = 3;
-constexpr int kThreadsDense = 320;  // TMA producer, MMA issuer, 8 builder/epilogue warps
-// (two per lane quarter, each for half of the GQA group's heads)
+// builder warps per lane quarter, each for an equal share of the GQA group's heads
+// (profiles/r02/dense_split4_v70.jsonl, beta 140: G=4 one head per warp B=4 409 -> 400 us,
+// B=8 821 -> 812 vs two heads; G=5 split 4 ways (2,2,1,0) 894 -> 950 at B=8, so 2 ways)
+constexpr int dense_split(int G) { return (G == 4 || G == 8) ? 4 : (G >= 2 ? 2 : 1); }
+// TMA producer, MMA issuer, 4 * split builder/epilogue warps
+constexpr int dense_threads(int G) { return 64 + 128 * dense_split(G); }
 
 // MN-major, 128B-swizzled UMMA descriptor of a V tile read as A = V^T (M = d):
 // 64 d (128 B) contiguous, the next 64 d one box (16 KB) away (LBO); 8 token
@@ -41,7 +45,7 @@ inline size_t dense_smem_bytes(int G) {
 }
 
 template <int G>
-__global__ void __launch_bounds__(kThreadsDense, 2)  // <= 102 registers
+__global__ void __launch_bounds__(dense_threads(G), 2)
     attend_dense_tc_kernel(const __grid_constant__ Batch bt, const __grid_constant__ Maps vmaps, Ws ws) {
   constexpr int NP = (3 * G <= 16) ? 16 : 32;
   constexpr int kBBytes = 2 * NP * 128;  // B operand: NP rows x 128 tokens, two 64-token boxes
@@ -72,7 +76,7 @@ __global__ void __launch_bounds__(kThreadsDense, 2)  // <= 102 registers
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kDenseStages; ++i) { mbar_init(full_bar(i), 1); mbar_init(empty_bar(i), 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(bfull0 + 8u * i, 8); mbar_init(bfree0 + 8u * i, 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(bfull0 + 8u * i, 4 * dense_split(G)); mbar_init(bfree0 + 8u * i, 1); }
     mbar_init(accf, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -143,7 +147,8 @@ __global__ void __launch_bounds__(kThreadsDense, 2)  // <= 102 registers
     }
   } else {
     // ===================== builders / epilogue (lane quarter q, heads of half hf) =====================
-    constexpr int GH = (G + 1) / 2;  // heads per builder warp
+    constexpr int kSplit = dense_split(G);
+    constexpr int GH = (G + kSplit - 1) / kSplit;  // heads per builder warp
     const int quarter = warp & 3, hf = (warp - 2) >> 2;
     const int jb = hf * GH;  // this warp's heads: jb + jj < G, jj < GH
     const float k2 = bt.inv_sqrt_d * kLog2e;
@@ -274,7 +279,7 @@ __global__ void __launch_bounds__(kThreadsDense, 2)  // <= 102 registers
       const int nr = (int)warp_sum((float)nret[jj]);
       if (lane == 0) { s_l[quarter][j] = l; s_ns[quarter][j] = nsel[jj]; s_nr[quarter][j] = nr; }
     }
-    asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 builder warps
+    asm volatile("bar.sync 1, %0;" ::"n"(128 * kSplit) : "memory");  // the builder warps
     if (warp == 2 && lane < G) {
       const int j = lane;
       float l = 0.f;

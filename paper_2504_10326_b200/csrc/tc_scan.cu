@@ -147,7 +147,7 @@ int launch_dense(const Batch& bt, const tc::Maps& vmaps, const Ws& ws, cudaStrea
     cudaFuncSetAttribute(tc::attend_dense_tc_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
-  return launch_pdl("attend_dense_tc_kernel", tc::attend_dense_tc_kernel<G>, bt.total_chunks, tc::kThreadsDense,
+  return launch_pdl("attend_dense_tc_kernel", tc::attend_dense_tc_kernel<G>, bt.total_chunks, tc::dense_threads(G),
                     sm, st, bt, vmaps, ws);
 }
 
