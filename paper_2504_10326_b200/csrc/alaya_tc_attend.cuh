@@ -25,9 +25,10 @@ namespace tc {
 
 constexpr int kDenseStages = 3;
 // builder warps per lane quarter, each for an equal share of the GQA group's heads
-// (profiles/r02/dense_split4_v70.jsonl, beta 140: G=4 one head per warp B=4 409 -> 400 us,
-// B=8 821 -> 812 vs two heads; G=5 split 4 ways (2,2,1,0) 894 -> 950 at B=8, so 2 ways)
-constexpr int dense_split(int G) { return (G == 4 || G == 8) ? 4 : (G >= 2 ? 2 : 1); }
+// (profiles/r02/dense_split4_v70.jsonl, dense_split_g5_v71.jsonl, beta 140: G=4 one head per
+// warp B=4 409 -> 400 us, B=8 821 -> 812 vs two heads; G=5 at B=8: 2 ways 894, 3 ways (2,2,1)
+// 864, 4 ways (2,2,1,0) 950, 5 ways 916)
+constexpr int dense_split(int G) { return (G == 4 || G == 8) ? 4 : (G >= 5 ? 3 : (G >= 2 ? 2 : 1)); }
 // TMA producer, MMA issuer, 4 * split builder/epilogue warps
 constexpr int dense_threads(int G) { return 64 + 128 * dense_split(G); }
 
